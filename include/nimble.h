@@ -1,0 +1,264 @@
+/* nimble.h -- C ABI of the B200-native NIMBLE data path.
+ *
+ * One shared library, paper_2604_00317_b200/libnimble_b200.so, exports every
+ * symbol below.  No C++ or CUDA types cross this boundary: plain pointers,
+ * sizes and opaque handles; streams are passed as `void*` (a cudaStream_t).
+ * No call throws; every call returns a nimbleResult_t, and
+ * nimbleGetLastError() returns the message of the last failure on the calling
+ * thread.
+ *
+ * Three groups, each mirroring an existing interface:
+ *
+ *  1. Link-load model, traffic-matrix ingest and planner -- the reference's
+ *     C++ planning API (/root/reference/proj/include/nimble/ headers), same
+ *     semantics, bit-exact results; host-only, usable without a GPU.
+ *  2. Communicator and data path -- shaped like NCCL 2.28.9's nccl.h (the
+ *     interface the paper says NIMBLE sits behind): result
+ *     codes nccl.h:42-50, data types nccl.h:300-313, unique id nccl.h:157,
+ *     ncclCommInitRank nccl.h:171, ncclCommInitAll nccl.h:180,
+ *     ncclCommDestroy nccl.h:192, ncclSend/ncclRecv nccl.h:507,526,
+ *     ncclGroupStart/End nccl.h:558,568, ncclAlltoAll nccl.h:460-461,
+ *     ncclCommRegister/Deregister, ncclMemAlloc/Free.
+ *  3. Benchmark entry points mirroring the artifact's --p2p / --skewed runs
+ *     (proj/tools/nimble.cpp:220-284) on real buffers.
+ */
+#ifndef NIMBLE_B200_H_
+#define NIMBLE_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NIMBLE_MAJOR 0
+#define NIMBLE_MINOR 1
+#define NIMBLE_PATCH 0
+#define NIMBLE_VERSION_CODE (NIMBLE_MAJOR * 10000 + NIMBLE_MINOR * 100 + NIMBLE_PATCH)
+
+/* Mirrors ncclResult_t (nccl.h:42-50). */
+typedef enum {
+    nimbleSuccess = 0,
+    nimbleUnhandledCudaError = 1,
+    nimbleSystemError = 2,
+    nimbleInternalError = 3,
+    nimbleInvalidArgument = 4,
+    nimbleInvalidUsage = 5,
+    nimbleRemoteError = 6,
+    nimbleInProgress = 7,
+    nimbleNumResults = 8
+} nimbleResult_t;
+
+/* Mirrors ncclDataType_t (nccl.h:300-313); only the element size matters. */
+typedef enum {
+    nimbleInt8 = 0, nimbleChar = 0,
+    nimbleUint8 = 1,
+    nimbleInt32 = 2, nimbleInt = 2,
+    nimbleUint32 = 3,
+    nimbleInt64 = 4,
+    nimbleUint64 = 5,
+    nimbleFloat16 = 6, nimbleHalf = 6,
+    nimbleFloat32 = 7, nimbleFloat = 7,
+    nimbleFloat64 = 8, nimbleDouble = 8,
+    nimbleBfloat16 = 9,
+    nimbleFloat8e4m3 = 10,
+    nimbleFloat8e5m2 = 11,
+    nimbleNumTypes = 12
+} nimbleDataType_t;
+
+const char* nimbleGetErrorString(nimbleResult_t result);
+const char* nimbleGetLastError(void);
+nimbleResult_t nimbleGetVersion(int* version);
+
+/* ------------------------------------------------------------------ 1. planning */
+
+/* proj/include/nimble/topology.hpp:36 (Fabric) */
+typedef enum { nimbleFabricAllToAll = 0, nimbleFabricNvSwitch = 1 } nimbleFabric_t;
+/* proj/include/nimble/topology.hpp:22 (LinkKind) */
+typedef enum { nimbleLinkNvLink = 0, nimbleLinkSwitchPort = 1, nimbleLinkAttach = 2, nimbleLinkRail = 3 } nimbleLinkKind_t;
+/* proj/include/nimble/planner.hpp:17 (PathClass) */
+typedef enum { nimbleRouteDirect = 0, nimbleRouteTwoHop = 1, nimbleRouteRail = 2 } nimbleRoute_t;
+
+typedef struct nimbleTopology* nimbleTopology_t;
+typedef struct nimblePlan* nimblePlan_t;
+
+/* replaces build_canonical (proj/include/nimble/topology.hpp:68-70, topology.cpp:119) */
+nimbleResult_t nimbleTopologyCreate(int nodes, int gpus_per_node, int nics_per_node,
+                                    double nvlink_bytes_per_s, double rail_bytes_per_s,
+                                    nimbleFabric_t fabric, nimbleTopology_t* topo);
+/* replaces load_topology / save_topology (topology.hpp:76-77) */
+nimbleResult_t nimbleTopologyLoad(const char* text, nimbleTopology_t* topo);
+nimbleResult_t nimbleTopologySave(nimbleTopology_t topo, char* out, size_t cap, size_t* need);
+nimbleResult_t nimbleTopologyDestroy(nimbleTopology_t topo);
+/* Topology::link_count / link(id) / link_name (topology.hpp:51-53) */
+nimbleResult_t nimbleTopologyLinkCount(nimbleTopology_t topo, int* count);
+nimbleResult_t nimbleTopologyLink(nimbleTopology_t topo, int id, int* kind, double* capacity,
+                                  char* name, size_t name_cap);
+/* per-link capacity override (the file format's "link <src> <dst> <gbps>") */
+nimbleResult_t nimbleTopologySetCapacity(nimbleTopology_t topo, int id, double bytes_per_s);
+/* Topology::port_up_id / port_down_id / nvlink_id (topology.hpp:57-59); -1 + error if absent */
+nimbleResult_t nimbleTopologyLinkId(nimbleTopology_t topo, int kind, int node, int a, int b, int* id);
+
+/* Traffic-matrix ingest: R*R row-major uint64 byte counts, row = sender.
+ * replaces gen_p2p / gen_skewed_a2av / gen_stencil_1d / gen_aggregator /
+ * gen_irregular (proj/include/nimble/workloads.hpp:39-56). */
+nimbleResult_t nimbleGenP2P(int ranks, int src, int dst, uint64_t size, uint64_t* matrix);
+nimbleResult_t nimbleGenSkewed(int ranks, uint64_t per_rank, double ratio, int hot_dst,
+                               int per_sender_hot, uint64_t* matrix);
+nimbleResult_t nimbleGenStencil1D(int ranks, uint64_t halo, uint64_t* matrix);
+nimbleResult_t nimbleGenAggregator(int ranks, const int* dsts, int ndsts, uint64_t per_src,
+                                   uint64_t* matrix);
+nimbleResult_t nimbleGenIrregular(int ranks, uint64_t total, double sparsity, uint64_t seed,
+                                  uint64_t* matrix);
+/* write_payload_matrix / read_payload_matrix (workloads.hpp:58-59); `ranks`
+ * in/out: capacity of `matrix` in entries on input, R on output. */
+nimbleResult_t nimbleMatrixToText(int ranks, const uint64_t* matrix, char* out, size_t cap, size_t* need);
+nimbleResult_t nimbleMatrixFromText(const char* text, uint64_t* matrix, size_t cap, int* ranks);
+
+/* proj/include/nimble/planner.hpp:36-56 (CostModel + PlannerConfig) */
+typedef struct {
+    double lambda;                 /* 0.5 */
+    uint64_t epsilon;              /* 4 MiB */
+    double pi;                     /* 0.25 */
+    uint64_t small_message_cutoff; /* 1 MiB */
+    uint64_t saturation_intra;     /* 64 MiB */
+    uint64_t saturation_inter;     /* 32 MiB */
+    uint64_t max_pair_visits;      /* 1e6 */
+    int normalize_by_capacity;     /* 1 */
+} nimblePlannerConfig;
+
+/* proj/include/nimble/planner.hpp:71-78 (PlanStats) */
+typedef struct {
+    uint64_t pair_visits, placements, fallback_pairs, residual_flows, refine_moves;
+    double wall_seconds;
+} nimblePlanStats;
+
+nimbleResult_t nimblePlannerConfigDefault(nimblePlannerConfig* cfg);
+/* replaces plan() (planner.hpp:99-100); ranks_per_node = RankMap block size */
+nimbleResult_t nimblePlanCreate(nimbleTopology_t topo, int ranks, int ranks_per_node,
+                                const uint64_t* matrix, const nimblePlannerConfig* cfg,
+                                nimblePlan_t* plan);
+/* replaces plan_direct_baseline() (planner.hpp:103-104) */
+nimbleResult_t nimblePlanDirect(nimbleTopology_t topo, int ranks, int ranks_per_node,
+                                const uint64_t* matrix, nimblePlan_t* plan);
+nimbleResult_t nimblePlanDestroy(nimblePlan_t plan);
+nimbleResult_t nimblePlanNumPairs(nimblePlan_t plan, int* npairs);
+nimbleResult_t nimblePlanPair(nimblePlan_t plan, int pair, int* src, int* dst, uint64_t* demand,
+                              int* ncandidates, int* nflows);
+/* enumerate_paths() output for the pair (planner.hpp:19-30,86-87) */
+nimbleResult_t nimblePlanCandidate(nimblePlan_t plan, int pair, int cand, int* route, int* via,
+                                   int* rail, int* hops, int* edges, int edges_cap, int* nedges);
+/* FlowAssignment (planner.hpp:58-61): the chunk-to-path assignment */
+nimbleResult_t nimblePlanFlow(nimblePlan_t plan, int pair, int flow, int* cand, double* bytes);
+nimbleResult_t nimblePlanGetStats(nimblePlan_t plan, nimblePlanStats* stats);
+/* plan_link_loads / max_normalized_load (planner.hpp:106-107) */
+nimbleResult_t nimblePlanLinkLoads(nimblePlan_t plan, double* loads, int nlinks);
+nimbleResult_t nimblePlanMaxNormalizedLoad(nimblePlan_t plan, double* seconds);
+/* plan_to_json (planner.hpp:109) */
+nimbleResult_t nimblePlanToJson(nimblePlan_t plan, char* out, size_t cap, size_t* need);
+
+/* ------------------------------------------------------------ 2. communicator */
+
+#define NIMBLE_UNIQUE_ID_BYTES 128
+typedef struct { char internal[NIMBLE_UNIQUE_ID_BYTES]; } nimbleUniqueId;
+typedef struct nimbleComm* nimbleComm_t;
+
+/* Runtime knobs of a communicator.  The planner runs on the comm's own
+ * link-load model: by default the B200 box as it is (nvswitch, 900 GB/s per
+ * port), which plans every pair direct; fabric = nimbleFabricAllToAll with
+ * gpus_per_node > nranks exercises the reference's mesh model, whose relay
+ * routes the forwarding engine then executes through peer staging rings. */
+typedef struct {
+    nimbleFabric_t fabric;        /* link-load model the planner charges     */
+    int gpus_per_node;            /* model GPUs (>= nranks); idle ones relay */
+    double nvlink_bytes_per_s;    /* per link / port                          */
+    nimblePlannerConfig planner;
+    uint64_t pipe_chunk;          /* relay staging slot size, 512 KiB (pipeline.hpp:19) */
+    uint64_t p2p_buffer;          /* staging bytes per ring, 10 MiB (pipeline.hpp:18)   */
+    int channels_per_peer;        /* rings per relayed flow, 1 (pipeline.hpp:23)        */
+    int ctas;                     /* forwarding-engine CTAs per launch, 0 = auto        */
+    uint64_t direct_chunk;        /* work-item size for direct pushes, 0 = auto         */
+} nimbleCommConfig;
+
+nimbleResult_t nimbleCommConfigDefault(nimbleCommConfig* cfg);
+
+nimbleResult_t nimbleGetUniqueId(nimbleUniqueId* uniqueId);
+/* One process per GPU (uses the calling thread's current CUDA device). */
+nimbleResult_t nimbleCommInitRank(nimbleComm_t* comm, int nranks, nimbleUniqueId commId, int rank);
+/* One process, `ndev` GPUs (devlist NULL = 0..ndev-1). */
+nimbleResult_t nimbleCommInitAll(nimbleComm_t* comms, int ndev, const int* devlist);
+nimbleResult_t nimbleCommDestroy(nimbleComm_t comm);
+nimbleResult_t nimbleCommCount(const nimbleComm_t comm, int* count);
+nimbleResult_t nimbleCommUserRank(const nimbleComm_t comm, int* rank);
+nimbleResult_t nimbleCommCuDevice(const nimbleComm_t comm, int* device);
+/* Device-side failures (flag-wait timeout, size mismatch) surface here. */
+nimbleResult_t nimbleCommGetAsyncError(nimbleComm_t comm, nimbleResult_t* asyncError);
+/* Collective across the comm; every rank must pass an equal config. */
+nimbleResult_t nimbleCommSetConfig(nimbleComm_t comm, const nimbleCommConfig* cfg);
+nimbleResult_t nimbleCommGetConfig(nimbleComm_t comm, nimbleCommConfig* cfg);
+
+/* Buffer registration (ncclCommRegister/Deregister).  Collective: every rank
+ * registers one buffer per call, in the same order.  Receive buffers inside a
+ * registered window are written in place by peers (zero copy); unregistered
+ * receive buffers are fed through the comm's staging rings. */
+nimbleResult_t nimbleCommRegister(const nimbleComm_t comm, void* buff, size_t size, void** handle);
+nimbleResult_t nimbleCommDeregister(const nimbleComm_t comm, void* handle);
+nimbleResult_t nimbleMemAlloc(void** ptr, size_t size);
+nimbleResult_t nimbleMemFree(void* ptr);
+
+nimbleResult_t nimbleGroupStart(void);
+nimbleResult_t nimbleGroupEnd(void);
+nimbleResult_t nimbleSend(const void* sendbuff, size_t count, nimbleDataType_t datatype, int peer,
+                          nimbleComm_t comm, void* stream);
+nimbleResult_t nimbleRecv(void* recvbuff, size_t count, nimbleDataType_t datatype, int peer,
+                          nimbleComm_t comm, void* stream);
+nimbleResult_t nimbleAlltoAll(const void* sendbuff, void* recvbuff, size_t count,
+                              nimbleDataType_t datatype, nimbleComm_t comm, void* stream);
+/* counts / displacements in elements of `datatype`, as MPI_Alltoallv */
+nimbleResult_t nimbleAlltoAllv(const void* sendbuff, const size_t sendcounts[], const size_t sdispls[],
+                               void* recvbuff, const size_t recvcounts[], const size_t rdispls[],
+                               nimbleDataType_t datatype, nimbleComm_t comm, void* stream);
+
+/* Single-GPU emulation of an R-rank exchange: one kernel moves every pair's
+ * segment (packed MPI layout) between R send and R receive buffers on the
+ * current device -- the 1-GPU local-copy calibration of the forwarding engine. */
+nimbleResult_t nimbleExchangeLocal(int ranks, const void* const* sendbuffs, void* const* recvbuffs,
+                                   const uint64_t* matrix, int ctas, void* stream);
+
+/* Payload helpers (device): byte j of pair (s,d) is byte j%8 of
+ * splitmix64(seed ^ s<<48 ^ d<<40 ^ j/8).  Check adds mismatching bytes into
+ * *mismatches (device pointer, uint64). */
+nimbleResult_t nimbleFillPayload(void* buf, uint64_t first, uint64_t nbytes, uint64_t seed, int src,
+                                 int dst, void* stream);
+nimbleResult_t nimbleCheckPayload(const void* buf, uint64_t first, uint64_t nbytes, uint64_t seed,
+                                  int src, int dst, uint64_t* mismatches, void* stream);
+
+/* --------------------------------------------------------- 3. bench entry points */
+
+typedef struct {
+    double seconds_median;   /* per exchange, max over ranks, CUDA events     */
+    double seconds_min;
+    double gbps_effective;   /* total payload bytes / seconds_median / 1e9    */
+    double bound_seconds;    /* MCF port bound of the matrix on this box      */
+    double plan_seconds;     /* host planner wall time for this matrix        */
+    uint64_t total_bytes;
+    uint64_t mismatches;     /* delivered bytes that differ from the payload  */
+    int relay_flows;         /* flows the plan routes through a relay          */
+} nimbleBenchResult;
+
+/* --p2p: `bytes` from src to dst (collective over the comm). */
+nimbleResult_t nimbleBenchP2P(nimbleComm_t comm, uint64_t bytes, int src, int dst, int warmup,
+                              int iters, nimbleBenchResult* result);
+/* --skewed: gen_skewed_a2av(nranks, per_rank, ratio, hot) (collective). */
+nimbleResult_t nimbleBenchSkewed(nimbleComm_t comm, uint64_t per_rank, double ratio, int hot,
+                                 int warmup, int iters, nimbleBenchResult* result);
+/* Any R*R matrix (packed layout), e.g. gen_irregular output (collective). */
+nimbleResult_t nimbleBenchMatrix(nimbleComm_t comm, const uint64_t* matrix, int warmup, int iters,
+                                 nimbleBenchResult* result);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NIMBLE_B200_H_ */

@@ -1,0 +1,228 @@
+// TCP rendezvous; see bootstrap.hpp.
+#include "bootstrap.hpp"
+
+#include <arpa/inet.h>
+#include <netinet/in.h>
+#include <netinet/tcp.h>
+#include <poll.h>
+#include <sys/socket.h>
+#include <unistd.h>
+
+#include <chrono>
+#include <cstdlib>
+#include <cstring>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <thread>
+
+#include "capi_util.hpp"
+
+namespace nb {
+
+namespace {
+
+constexpr uint32_t kMagic = 0x4e4d4231;  // "NMB1"
+constexpr int kIoTimeoutMs = 600000;     // a silent peer for 10 min is dead
+
+struct IdBlob {
+    uint32_t magic;
+    uint32_t addr;  // IPv4, network order
+    uint16_t port;  // network order
+    uint16_t pad;
+    uint64_t nonce;
+};
+static_assert(sizeof(IdBlob) <= NIMBLE_UNIQUE_ID_BYTES, "id blob too large");
+
+struct Hello {
+    uint32_t magic;
+    int32_t rank, nranks;
+    uint32_t pad;
+    uint64_t nonce;
+};
+
+[[noreturn]] void sys_fail(const std::string& what) {
+    throw Error(nimbleSystemError, "bootstrap: " + what + ": " + std::strerror(errno));
+}
+
+void wait_io(int fd, short ev) {
+    pollfd p{fd, ev, 0};
+    int r = ::poll(&p, 1, kIoTimeoutMs);
+    if (r == 0) throw Error(nimbleRemoteError, "bootstrap: peer timed out");
+    if (r < 0 && errno != EINTR) sys_fail("poll");
+}
+
+void send_all(int fd, const void* p, size_t n) {
+    auto* b = static_cast<const uint8_t*>(p);
+    while (n) {
+        wait_io(fd, POLLOUT);
+        ssize_t k = ::send(fd, b, n, MSG_NOSIGNAL);
+        if (k < 0) {
+            if (errno == EINTR || errno == EAGAIN) continue;
+            sys_fail("send");
+        }
+        b += k;
+        n -= static_cast<size_t>(k);
+    }
+}
+
+// false on orderly close before any byte
+bool recv_all(int fd, void* p, size_t n) {
+    auto* b = static_cast<uint8_t*>(p);
+    size_t got = 0;
+    while (got < n) {
+        wait_io(fd, POLLIN);
+        ssize_t k = ::recv(fd, b + got, n - got, 0);
+        if (k == 0) {
+            if (got == 0) return false;
+            throw Error(nimbleRemoteError, "bootstrap: peer closed mid-message");
+        }
+        if (k < 0) {
+            if (errno == EINTR || errno == EAGAIN) continue;
+            sys_fail("recv");
+        }
+        got += static_cast<size_t>(k);
+    }
+    return true;
+}
+
+void tune(int fd) {
+    int one = 1;
+    ::setsockopt(fd, IPPROTO_TCP, TCP_NODELAY, &one, sizeof one);
+}
+
+// Root service: accept nranks members, then run allgather rounds until every
+// member has closed its socket.
+void serve(int lfd, uint64_t nonce) {
+    std::vector<int> fds;
+    try {
+        int nranks = -1;
+        std::vector<std::pair<int, int>> joined;  // (rank, fd)
+        while (nranks < 0 || static_cast<int>(joined.size()) < nranks) {
+            wait_io(lfd, POLLIN);
+            int fd = ::accept(lfd, nullptr, nullptr);
+            if (fd < 0) {
+                if (errno == EINTR) continue;
+                sys_fail("accept");
+            }
+            tune(fd);
+            Hello h{};
+            if (!recv_all(fd, &h, sizeof h) || h.magic != kMagic || h.nonce != nonce) {
+                ::close(fd);
+                continue;
+            }
+            if (nranks < 0) nranks = h.nranks;
+            if (h.nranks != nranks || h.rank < 0 || h.rank >= nranks) {
+                ::close(fd);
+                continue;
+            }
+            joined.push_back({h.rank, fd});
+        }
+        fds.assign(static_cast<size_t>(nranks), -1);
+        for (auto& [r, fd] : joined) fds[static_cast<size_t>(r)] = fd;
+        for (int fd : fds)
+            if (fd < 0) throw Error(nimbleInternalError, "bootstrap: duplicate rank");
+        for (;;) {
+            std::vector<uint8_t> all;
+            uint64_t n = 0;
+            bool closed = false;
+            for (size_t r = 0; r < fds.size(); ++r) {
+                uint64_t len = 0;
+                if (!recv_all(fds[r], &len, sizeof len)) {
+                    closed = true;
+                    break;
+                }
+                if (r == 0) {
+                    n = len;
+                    all.resize(n * fds.size());
+                } else if (len != n) {
+                    throw Error(nimbleInvalidUsage, "bootstrap: allgather sizes differ across ranks");
+                }
+                if (n && !recv_all(fds[r], all.data() + r * n, n))
+                    throw Error(nimbleRemoteError, "bootstrap: short allgather");
+            }
+            if (closed) break;
+            for (int fd : fds) send_all(fd, all.data(), all.size());
+        }
+    } catch (...) {
+    }
+    for (int fd : fds)
+        if (fd >= 0) ::close(fd);
+    ::close(lfd);
+}
+
+class TcpBootstrap final : public Bootstrap {
+  public:
+    TcpBootstrap(const IdBlob& id, int r, int n) {
+        rank = r;
+        nranks = n;
+        sockaddr_in sa{};
+        sa.sin_family = AF_INET;
+        sa.sin_addr.s_addr = id.addr;
+        sa.sin_port = id.port;
+        const auto deadline = std::chrono::steady_clock::now() + std::chrono::seconds(120);
+        for (;;) {
+            fd_ = ::socket(AF_INET, SOCK_STREAM, 0);
+            if (fd_ < 0) sys_fail("socket");
+            if (::connect(fd_, reinterpret_cast<sockaddr*>(&sa), sizeof sa) == 0) break;
+            ::close(fd_);
+            fd_ = -1;
+            if (std::chrono::steady_clock::now() > deadline)
+                throw Error(nimbleRemoteError, "bootstrap: cannot reach the root");
+            std::this_thread::sleep_for(std::chrono::milliseconds(20));
+        }
+        tune(fd_);
+        Hello h{kMagic, r, n, 0, id.nonce};
+        send_all(fd_, &h, sizeof h);
+    }
+    ~TcpBootstrap() override {
+        if (fd_ >= 0) ::close(fd_);
+    }
+    void allgather(const void* mine, size_t n, void* all) override {
+        uint64_t len = n;
+        send_all(fd_, &len, sizeof len);
+        if (n) send_all(fd_, mine, n);
+        if (!recv_all(fd_, all, n * static_cast<size_t>(nranks)) && n)
+            throw Error(nimbleRemoteError, "bootstrap: root closed");
+    }
+
+  private:
+    int fd_ = -1;
+};
+
+}  // namespace
+
+void bootstrap_root(nimbleUniqueId* id) {
+    const char* env = std::getenv("NIMBLE_BOOTSTRAP_ADDR");
+    in_addr addr{};
+    if (::inet_pton(AF_INET, env && *env ? env : "127.0.0.1", &addr) != 1)
+        throw Error(nimbleInvalidArgument, "bootstrap: bad NIMBLE_BOOTSTRAP_ADDR");
+    int lfd = ::socket(AF_INET, SOCK_STREAM, 0);
+    if (lfd < 0) sys_fail("socket");
+    int one = 1;
+    ::setsockopt(lfd, SOL_SOCKET, SO_REUSEADDR, &one, sizeof one);
+    sockaddr_in sa{};
+    sa.sin_family = AF_INET;
+    sa.sin_addr = addr;
+    sa.sin_port = 0;
+    if (::bind(lfd, reinterpret_cast<sockaddr*>(&sa), sizeof sa) != 0) sys_fail("bind");
+    if (::listen(lfd, 256) != 0) sys_fail("listen");
+    socklen_t sl = sizeof sa;
+    if (::getsockname(lfd, reinterpret_cast<sockaddr*>(&sa), &sl) != 0) sys_fail("getsockname");
+    std::random_device rd;
+    const uint64_t nonce = (static_cast<uint64_t>(rd()) << 32) ^ rd() ^ static_cast<uint64_t>(::getpid());
+    IdBlob blob{kMagic, addr.s_addr, sa.sin_port, 0, nonce};
+    std::memset(id, 0, sizeof *id);
+    std::memcpy(id->internal, &blob, sizeof blob);
+    std::thread(serve, lfd, nonce).detach();
+}
+
+std::unique_ptr<Bootstrap> bootstrap_connect(const nimbleUniqueId& id, int rank, int nranks) {
+    IdBlob blob;
+    std::memcpy(&blob, id.internal, sizeof blob);
+    if (blob.magic != kMagic) throw Error(nimbleInvalidArgument, "bootstrap: not a nimble unique id");
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(nimbleInvalidArgument, "bootstrap: bad rank");
+    return std::make_unique<TcpBootstrap>(blob, rank, nranks);
+}
+
+}  // namespace nb

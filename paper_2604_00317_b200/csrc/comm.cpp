@@ -1,0 +1,1078 @@
+// C ABI, groups 2 and 3: communicator, registration, group semantics,
+// send/recv / all-to-all(v), the 1-GPU emulated exchange and the bench entry
+// points.  Host C++ around the sm_100a forwarding engine (engine.cu).
+//
+// Per call (stream-ordered, asynchronous, NCCL-style):
+//   1. the group's ops become per-peer send / receive segments;
+//   2. the planner runs on the comm's link-load model -- replicated on every
+//      rank; the nvswitch model needs only this rank's row and column, the
+//      mesh model gathers the full R x R matrix over the bootstrap;
+//   3. the chunk scheduler turns plan + buffers into this rank's item list
+//      (plan and schedule are cached, so a repeated exchange re-launches with
+//      zero host work beyond the launch);
+//   4. one forwarding-engine launch per rank.
+#include <cuda_runtime.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <list>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/nimble.h"
+#include "bootstrap.hpp"
+#include "capi_util.hpp"
+#include "demand.hpp"
+#include "device.cuh"
+#include "fabric.hpp"
+#include "planner.hpp"
+#include "schedule.hpp"
+
+namespace nb {
+cudaError_t launch_exchange(const LaunchArgs& args, int ctas, cudaStream_t stream);
+cudaError_t launch_fill(void* buf, uint64_t first, uint64_t n, uint64_t seed, int s, int d, cudaStream_t st);
+cudaError_t launch_check(const void* buf, uint64_t first, uint64_t n, uint64_t seed, int s, int d, uint64_t* bad,
+                         cudaStream_t st);
+PlanParams to_params(const nimblePlannerConfig* c);
+}  // namespace nb
+
+#define CUDA_TRY(x)                                                                                            \
+    do {                                                                                                       \
+        cudaError_t e_ = (x);                                                                                  \
+        if (e_ != cudaSuccess)                                                                                 \
+            throw nb::Error(nimbleUnhandledCudaError, std::string(#x) + ": " + cudaGetErrorString(e_));       \
+    } while (0)
+
+namespace nb {
+namespace {
+
+using GetRangeFn = int (*)(unsigned long long*, size_t*, unsigned long long);
+
+GetRangeFn address_range_fn() {
+    static GetRangeFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess)
+            return static_cast<GetRangeFn>(nullptr);
+        return reinterpret_cast<GetRangeFn>(p);
+    }();
+    return fn;
+}
+
+// allocation containing `ptr` (base, size)
+std::pair<uint64_t, uint64_t> allocation_of(const void* ptr) {
+    GetRangeFn fn = address_range_fn();
+    if (!fn) throw Error(nimbleSystemError, "cuMemGetAddressRange unavailable");
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (fn(&base, &size, reinterpret_cast<unsigned long long>(ptr)) != 0)
+        throw Error(nimbleInvalidArgument, "register: pointer is not device memory");
+    return {base, size};
+}
+
+uint64_t fnv(const void* p, size_t n, uint64_t h = 1469598103934665603ull) {
+    auto* b = static_cast<const uint8_t*>(p);
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+    return h;
+}
+
+size_t elem_size(nimbleDataType_t t) {
+    switch (t) {
+    case nimbleInt8:
+    case nimbleUint8:
+    case nimbleFloat8e4m3:
+    case nimbleFloat8e5m2: return 1;
+    case nimbleFloat16:
+    case nimbleBfloat16: return 2;
+    case nimbleInt32:
+    case nimbleUint32:
+    case nimbleFloat32: return 4;
+    case nimbleInt64:
+    case nimbleUint64:
+    case nimbleFloat64: return 8;
+    default: throw Error(nimbleInvalidArgument, "bad datatype");
+    }
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) CUDA_TRY(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p, n = o.n;
+            o.p = nullptr, o.n = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void assign(const std::vector<T>& v, cudaStream_t st) {
+        if (v.size() > n) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            CUDA_TRY(cudaMalloc(&p, std::max<size_t>(v.size(), 1) * sizeof(T)));
+            n = v.size();
+        }
+        if (!v.empty()) CUDA_TRY(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+struct PeerInfo {
+    int32_t pid;
+    int32_t dev;
+    uint64_t host;
+    cudaIpcMemHandle_t ctrl, staging;
+};
+
+struct Window {
+    bool live = false;
+    uint64_t base = 0, size = 0;  // registered range (local)
+    std::vector<void*> opened;    // IPC mappings to close
+};
+
+struct CachedPlan {
+    std::vector<uint64_t> key;
+    std::shared_ptr<PlanResult> plan;
+    uint64_t id = 0;
+    double seconds = 0;
+};
+
+struct CachedSchedule {
+    std::vector<uint64_t> key;
+    Schedule sc;
+    DevBuf<Item> items;
+    DevBuf<Post> posts;
+    DevBuf<uint64_t> finals;
+};
+
+struct Clique;
+
+// Process-wide cache of opened IPC handles: one allocation may back several
+// registered windows, and a handle may be opened only once per process.
+struct IpcCache {
+    std::mutex m;
+    std::map<std::string, std::pair<void*, int>> open;  // handle bytes -> (base, refs)
+    void* acquire(const cudaIpcMemHandle_t& h) {
+        std::lock_guard<std::mutex> g(m);
+        std::string k(reinterpret_cast<const char*>(&h), sizeof h);
+        auto it = open.find(k);
+        if (it != open.end()) {
+            ++it->second.second;
+            return it->second.first;
+        }
+        void* p = nullptr;
+        CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        open[k] = {p, 1};
+        return p;
+    }
+    void release(void* p) {
+        std::lock_guard<std::mutex> g(m);
+        for (auto it = open.begin(); it != open.end(); ++it)
+            if (it->second.first == p) {
+                if (--it->second.second == 0) {
+                    cudaIpcCloseMemHandle(p);
+                    open.erase(it);
+                }
+                return;
+            }
+    }
+};
+
+IpcCache& ipc_cache() {
+    static IpcCache c;
+    return c;
+}
+
+}  // namespace
+}  // namespace nb
+
+struct nimbleComm {
+    int rank = 0, nranks = 1, device = 0, sms = 148;
+    std::unique_ptr<nb::Bootstrap> boot;
+    std::shared_ptr<nb::Clique> clique;
+    nimbleCommConfig cfg{};
+    uint8_t* ctrl = nullptr;
+    uint8_t* staging = nullptr;
+    uint64_t staging_bytes = 0;
+    std::vector<uint8_t*> peer_ctrl, peer_staging;
+    std::vector<void*> ipc_mapped;  // ctrl / staging mappings of peers
+    nb::CommDevice view{};
+    nb::CommDevice* d_view = nullptr;
+    uint64_t* d_win_table = nullptr;
+    uint32_t* d_scratch = nullptr;
+    uint32_t* h_status = nullptr;  // host-mapped async error word
+    uint32_t* d_status = nullptr;  // its device alias
+    std::vector<nb::Window> windows;
+    std::vector<uint64_t> win_table;  // [win * kMaxRanks + rank]
+    uint64_t epoch = 0;
+    uint64_t plan_ids = 0;
+    std::list<nb::CachedPlan> plans;
+    std::list<nb::CachedSchedule> schedules;
+    cudaStream_t bench_stream = nullptr;
+};
+
+namespace nb {
+namespace {
+
+struct Clique {
+    std::vector<nimbleComm*> comms;
+};
+
+void upload_view(nimbleComm* c) {
+    c->view.rank = c->rank;
+    c->view.nranks = c->nranks;
+    for (int r = 0; r < c->nranks; ++r) {
+        c->view.ctrl[r] = c->peer_ctrl[static_cast<size_t>(r)];
+        c->view.staging[r] = c->peer_staging[static_cast<size_t>(r)];
+    }
+    c->view.win_table = c->d_win_table;
+    c->view.nwin = static_cast<uint32_t>(c->windows.size());
+    c->view.status = c->d_status;
+    c->view.scratch = c->d_scratch;
+    const char* t = std::getenv("NIMBLE_TIMEOUT_MS");
+    c->view.timeout_ms = t && *t ? static_cast<uint32_t>(std::atoi(t)) : 20000u;
+    CUDA_TRY(cudaMemcpy(c->d_view, &c->view, sizeof c->view, cudaMemcpyHostToDevice));
+}
+
+constexpr uint32_t kMaxWindows = 256;
+
+uint32_t slot_count(const nimbleCommConfig& cfg) {
+    if (cfg.pipe_chunk == 0) throw Error(nimbleInvalidArgument, "config: pipe_chunk must be positive");
+    const uint64_t s = static_cast<uint64_t>(cfg.channels_per_peer) * (cfg.p2p_buffer / cfg.pipe_chunk);
+    if (s == 0) throw Error(nimbleInvalidArgument, "config: p2p_buffer holds less than one chunk");
+    if (s > kMaxSlots) throw Error(nimbleInvalidArgument, "config: more than 64 staging slots per ring");
+    return static_cast<uint32_t>(s);
+}
+
+uint64_t staging_size(const nimbleComm* c) {
+    return static_cast<uint64_t>(c->nranks) * c->nranks * slot_count(c->cfg) * c->cfg.pipe_chunk;
+}
+
+void default_config(nimbleCommConfig* cfg, int nranks) {
+    std::memset(cfg, 0, sizeof *cfg);
+    cfg->fabric = nimbleFabricNvSwitch;
+    cfg->gpus_per_node = nranks;
+    cfg->nvlink_bytes_per_s = 900e9;
+    nimblePlannerConfigDefault(&cfg->planner);
+    cfg->pipe_chunk = 512ull << 10;
+    cfg->p2p_buffer = 10ull << 20;
+    cfg->channels_per_peer = 1;
+    cfg->ctas = 0;
+    cfg->direct_chunk = 0;
+}
+
+// Allocate ctrl + staging, exchange handles / pointers, map peers.
+void setup_regions(nimbleComm* c, bool single_process) {
+    DeviceGuard g(c->device);
+    c->staging_bytes = staging_size(c);
+    const uint64_t ctrl_bytes = FlagLayout::bytes(c->nranks);
+    CUDA_TRY(cudaMalloc(&c->ctrl, ctrl_bytes));
+    CUDA_TRY(cudaMemset(c->ctrl, 0, ctrl_bytes));
+    CUDA_TRY(cudaMalloc(&c->staging, std::max<uint64_t>(c->staging_bytes, 256)));
+    c->peer_ctrl.assign(static_cast<size_t>(c->nranks), nullptr);
+    c->peer_staging.assign(static_cast<size_t>(c->nranks), nullptr);
+    c->peer_ctrl[static_cast<size_t>(c->rank)] = c->ctrl;
+    c->peer_staging[static_cast<size_t>(c->rank)] = c->staging;
+    if (single_process) return;  // the clique fills peers in directly
+    PeerInfo mine{};
+    mine.pid = ::getpid();
+    mine.dev = c->device;
+    mine.host = ::gethostid();
+    CUDA_TRY(cudaIpcGetMemHandle(&mine.ctrl, c->ctrl));
+    CUDA_TRY(cudaIpcGetMemHandle(&mine.staging, c->staging));
+    std::vector<PeerInfo> all(static_cast<size_t>(c->nranks));
+    c->boot->allgather(&mine, sizeof mine, all.data());
+    for (int r = 0; r < c->nranks; ++r) {
+        if (r == c->rank) continue;
+        const PeerInfo& p = all[static_cast<size_t>(r)];
+        if (p.host != mine.host) throw Error(nimbleInvalidUsage, "comm: ranks must share one NVLink box");
+        void* a = nullptr;
+        void* b = nullptr;
+        CUDA_TRY(cudaIpcOpenMemHandle(&a, p.ctrl, cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_mapped.push_back(a);
+        CUDA_TRY(cudaIpcOpenMemHandle(&b, p.staging, cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_mapped.push_back(b);
+        c->peer_ctrl[static_cast<size_t>(r)] = static_cast<uint8_t*>(a);
+        c->peer_staging[static_cast<size_t>(r)] = static_cast<uint8_t*>(b);
+    }
+}
+
+void setup_common(nimbleComm* c) {
+    DeviceGuard g(c->device);
+    CUDA_TRY(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
+    CUDA_TRY(cudaMalloc(&c->d_view, sizeof(CommDevice)));
+    CUDA_TRY(cudaMalloc(&c->d_win_table, sizeof(uint64_t) * kMaxWindows * kMaxRanks));
+    CUDA_TRY(cudaMemset(c->d_win_table, 0, sizeof(uint64_t) * kMaxWindows * kMaxRanks));
+    CUDA_TRY(cudaMalloc(&c->d_scratch, sizeof(uint32_t) * (2 + kMaxRanks)));
+    CUDA_TRY(cudaMemset(c->d_scratch, 0, sizeof(uint32_t) * (2 + kMaxRanks)));
+    CUDA_TRY(cudaHostAlloc(&c->h_status, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+    std::memset(c->h_status, 0, 64);
+    CUDA_TRY(cudaHostGetDevicePointer(&c->d_status, c->h_status, 0));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->bench_stream, cudaStreamNonBlocking));
+    c->win_table.assign(static_cast<size_t>(kMaxWindows) * kMaxRanks, 0);
+}
+
+void free_regions(nimbleComm* c) {
+    DeviceGuard g(c->device);
+    for (void* p : c->ipc_mapped) cudaIpcCloseMemHandle(p);
+    c->ipc_mapped.clear();
+    if (c->ctrl) cudaFree(c->ctrl);
+    if (c->staging) cudaFree(c->staging);
+    c->ctrl = c->staging = nullptr;
+}
+
+// ---------------------------------------------------------------- planning
+
+LinkModel comm_model(const nimbleComm* c) {
+    const int gpn = std::max(c->cfg.gpus_per_node, c->nranks);
+    const FabricKind f = c->cfg.fabric == nimbleFabricAllToAll ? FabricKind::AllToAll : FabricKind::NvSwitch;
+    return make_link_model(1, gpn, 0, c->cfg.nvlink_bytes_per_s, 0.0, f);
+}
+
+std::shared_ptr<PlanResult> plan_for(nimbleComm* c, const std::vector<uint64_t>& matrix, uint64_t* plan_id) {
+    std::vector<uint64_t> key = matrix;
+    key.push_back(fnv(&c->cfg, sizeof c->cfg));
+    for (auto it = c->plans.begin(); it != c->plans.end(); ++it)
+        if (it->key == key) {
+            c->plans.splice(c->plans.begin(), c->plans, it);
+            *plan_id = it->id;
+            return it->plan;
+        }
+    const LinkModel lm = comm_model(c);
+    Demand d;
+    d.ranks = c->nranks;
+    d.bytes = matrix;
+    auto p = std::make_shared<PlanResult>(mcf_plan(lm, c->nranks, lm.gpus, d, to_params(&c->cfg.planner)));
+    c->plans.push_front({key, p, ++c->plan_ids, p->stats.wall_seconds});
+    if (c->plans.size() > 4) c->plans.pop_back();
+    *plan_id = c->plan_ids;
+    return p;
+}
+
+// ---------------------------------------------------------------- groups
+
+struct PendingOp {
+    enum Kind { Send, Recv, AllToAllV } kind;
+    nimbleComm* comm;
+    cudaStream_t stream;
+    int peer;
+    uint64_t ptr, bytes;                                      // Send / Recv
+    uint64_t sbase, rbase;                                    // AllToAllV
+    std::vector<uint64_t> sbytes, soff, rbytes, roff;         // AllToAllV (bytes)
+};
+
+thread_local int g_group_depth = 0;
+thread_local std::vector<PendingOp> g_pending;
+
+struct Exchange {
+    nimbleComm* comm;
+    cudaStream_t stream;
+    std::vector<cudaStream_t> others;
+    RankBuffers rb;
+    std::vector<bool> has_send, has_recv;
+};
+
+Exchange make_exchange(nimbleComm* c, const std::vector<PendingOp*>& ops) {
+    Exchange ex;
+    ex.comm = c;
+    ex.stream = ops.front()->stream;
+    const int R = c->nranks;
+    ex.rb.R = R;
+    ex.rb.me = c->rank;
+    ex.rb.send_ptr.assign(R, 0);
+    ex.rb.send_bytes.assign(R, 0);
+    ex.rb.recv_ptr.assign(R, 0);
+    ex.rb.recv_bytes.assign(R, 0);
+    ex.has_send.assign(R, false);
+    ex.has_recv.assign(R, false);
+    auto set_send = [&](int p, uint64_t ptr, uint64_t n) {
+        if (ex.has_send[p]) throw Error(nimbleInvalidUsage, "group: two sends to one peer");
+        ex.has_send[p] = true;
+        ex.rb.send_ptr[p] = ptr;
+        ex.rb.send_bytes[p] = n;
+    };
+    auto set_recv = [&](int p, uint64_t ptr, uint64_t n) {
+        if (ex.has_recv[p]) throw Error(nimbleInvalidUsage, "group: two receives from one peer");
+        ex.has_recv[p] = true;
+        ex.rb.recv_ptr[p] = ptr;
+        ex.rb.recv_bytes[p] = n;
+    };
+    for (PendingOp* op : ops) {
+        if (op->stream != ex.stream &&
+            std::find(ex.others.begin(), ex.others.end(), op->stream) == ex.others.end())
+            ex.others.push_back(op->stream);
+        if (op->kind == PendingOp::Send) set_send(op->peer, op->ptr, op->bytes);
+        else if (op->kind == PendingOp::Recv) set_recv(op->peer, op->ptr, op->bytes);
+        else
+            for (int p = 0; p < R; ++p) {
+                set_send(p, op->sbase + op->soff[p], op->sbytes[p]);
+                set_recv(p, op->rbase + op->roff[p], op->rbytes[p]);
+            }
+    }
+    return ex;
+}
+
+// Where each incoming segment lands: a registered window (zero copy) or the
+// self ring (staged).
+void fill_posts(nimbleComm* c, RankBuffers& rb) {
+    rb.recv_post.assign(static_cast<size_t>(rb.R), Post{});
+    for (int s = 0; s < rb.R; ++s) {
+        if (s == rb.me || rb.recv_bytes[s] == 0) continue;
+        Post p{};
+        p.tag = 1;
+        p.bytes = rb.recv_bytes[s];
+        p.mode = kPostStaged;
+        p.off = rb.recv_ptr[s];
+        for (size_t w = 0; w < c->windows.size(); ++w) {
+            const Window& win = c->windows[w];
+            if (win.live && rb.recv_ptr[s] >= win.base && rb.recv_ptr[s] + rb.recv_bytes[s] <= win.base + win.size) {
+                p.mode = kPostZeroCopy;
+                p.win = static_cast<uint32_t>(w);
+                p.off = rb.recv_ptr[s] - win.base;
+                break;
+            }
+        }
+        rb.recv_post[static_cast<size_t>(s)] = p;
+    }
+}
+
+CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& plan, const RankBuffers& rb,
+                             cudaStream_t st) {
+    std::vector<uint64_t> key = {plan_id, c->cfg.pipe_chunk, c->cfg.p2p_buffer,
+                                 static_cast<uint64_t>(c->cfg.channels_per_peer), c->cfg.direct_chunk};
+    for (int r = 0; r < rb.R; ++r) {
+        key.push_back(rb.send_ptr[r]);
+        key.push_back(rb.send_bytes[r]);
+        key.push_back(rb.recv_ptr[r]);
+        key.push_back(rb.recv_bytes[r]);
+        key.push_back(rb.recv_post[r].mode);
+        key.push_back(rb.recv_post[r].win);
+    }
+    for (auto it = c->schedules.begin(); it != c->schedules.end(); ++it)
+        if (it->key == key) {
+            c->schedules.splice(c->schedules.begin(), c->schedules, it);
+            return c->schedules.front();
+        }
+    CachedSchedule cs;
+    cs.key = key;
+    const uint64_t local_chunk = c->cfg.direct_chunk ? c->cfg.direct_chunk : (1ull << 20);
+    cs.sc = build_schedule(plan, rb, c->cfg.pipe_chunk, slot_count(c->cfg), local_chunk);
+    if (c->schedules.size() >= 4) {  // recycle the oldest entry's device buffers
+        CUDA_TRY(cudaDeviceSynchronize());  // no launch may still read them
+        CachedSchedule& old = c->schedules.back();
+        cs.items = std::move(old.items);
+        cs.posts = std::move(old.posts);
+        cs.finals = std::move(old.finals);
+        c->schedules.pop_back();
+    }
+    cs.items.assign(cs.sc.items, st);
+    cs.posts.assign(cs.sc.posts, st);
+    cs.finals.assign(cs.sc.final_waits, st);
+    c->schedules.push_front(std::move(cs));
+    return c->schedules.front();
+}
+
+void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream_t st) {
+    LaunchArgs a{};
+    a.items = cs.items.p;
+    a.nitems = static_cast<uint32_t>(cs.sc.items.size());
+    a.slots = slot_count(c->cfg);
+    a.pipe_chunk = c->cfg.pipe_chunk;
+    a.epoch = ++c->epoch;
+    a.comm = c->d_view;
+    a.posts = cs.posts.p;
+    for (int r = 0; r < c->nranks; ++r) {
+        a.push_items[r] = cs.sc.push_items[r];
+        a.fwd_items[r] = cs.sc.fwd_items[r];
+        a.send_bytes[r] = rb.send_bytes[r];
+    }
+    a.expect_done = cs.sc.expect_done;
+    a.final_waits = cs.finals.p;
+    a.nfinal = static_cast<uint32_t>(cs.sc.final_waits.size() / 2);
+    a.local_only = 0;
+    int ctas = c->cfg.ctas > 0 ? c->cfg.ctas : c->sms;
+    ctas = std::max(1, std::min(ctas, c->sms));
+    // every rank launches even with nothing to move: its posts and done
+    // flags are what its peers wait for
+    CUDA_TRY(launch_exchange(a, ctas, st));
+}
+
+void run_exchanges(std::vector<Exchange>& exs) {
+    // full demand matrix when the planner's model can route through relays
+    std::map<nimbleComm*, std::vector<uint64_t>> full;
+    for (Exchange& ex : exs) {
+        nimbleComm* c = ex.comm;
+        const int R = c->nranks;
+        if (c->cfg.fabric != nimbleFabricAllToAll) continue;
+        std::vector<uint64_t> m(static_cast<size_t>(R) * R, 0);
+        if (c->boot) {
+            std::vector<uint64_t> row(ex.rb.send_bytes);
+            c->boot->allgather(row.data(), row.size() * sizeof(uint64_t), m.data());
+        } else {
+            for (Exchange& other : exs)
+                if (other.comm->clique == c->clique)
+                    for (int d = 0; d < R; ++d) m[static_cast<size_t>(other.comm->rank) * R + d] = other.rb.send_bytes[d];
+            for (nimbleComm* peer : c->clique->comms) {
+                bool present = false;
+                for (Exchange& other : exs) present |= other.comm == peer;
+                if (!present) throw Error(nimbleInvalidUsage, "group: every comm of the clique must take part");
+            }
+        }
+        full[c] = std::move(m);
+    }
+    for (Exchange& ex : exs) {
+        nimbleComm* c = ex.comm;
+        DeviceGuard g(c->device);
+        const int R = c->nranks, me = c->rank;
+        std::vector<uint64_t> m;
+        if (full.count(c)) {
+            m = full[c];
+        } else {  // nvswitch: one route per pair, my row and column decide my part
+            m.assign(static_cast<size_t>(R) * R, 0);
+            for (int p = 0; p < R; ++p) {
+                if (p == me) continue;
+                m[static_cast<size_t>(me) * R + p] = ex.rb.send_bytes[p];
+                m[static_cast<size_t>(p) * R + me] = ex.rb.recv_bytes[p];
+            }
+        }
+        for (int p = 0; p < R; ++p) m[static_cast<size_t>(p) * R + p] = 0;
+        uint64_t plan_id = 0;
+        std::shared_ptr<PlanResult> plan = plan_for(c, m, &plan_id);
+        fill_posts(c, ex.rb);
+        CachedSchedule& cs = schedule_for(c, plan_id, *plan, ex.rb, ex.stream);
+        std::vector<cudaEvent_t> evs;
+        for (cudaStream_t o : ex.others) {
+            cudaEvent_t e;
+            CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            CUDA_TRY(cudaEventRecord(e, o));
+            CUDA_TRY(cudaStreamWaitEvent(ex.stream, e, 0));
+            evs.push_back(e);
+        }
+        launch(c, cs, ex.rb, ex.stream);
+        for (size_t i = 0; i < ex.others.size(); ++i) {
+            CUDA_TRY(cudaEventRecord(evs[i], ex.stream));
+            CUDA_TRY(cudaStreamWaitEvent(ex.others[i], evs[i], 0));
+            cudaEventDestroy(evs[i]);
+        }
+    }
+}
+
+void flush_group() {
+    std::vector<PendingOp> ops;
+    ops.swap(g_pending);
+    std::vector<nimbleComm*> order;
+    std::map<nimbleComm*, std::vector<PendingOp*>> by_comm;
+    for (PendingOp& op : ops) {
+        if (!by_comm.count(op.comm)) order.push_back(op.comm);
+        by_comm[op.comm].push_back(&op);
+    }
+    std::vector<Exchange> exs;
+    for (nimbleComm* c : order) exs.push_back(make_exchange(c, by_comm[c]));
+    run_exchanges(exs);
+}
+
+nimbleResult_t enqueue(PendingOp&& op) {
+    return guarded([&] {
+        if (!op.comm) throw Error(nimbleInvalidArgument, "null comm");
+        g_pending.push_back(std::move(op));
+        if (g_group_depth == 0) flush_group();
+    });
+}
+
+// ---------------------------------------------------------------- registration
+
+void* register_window(nimbleComm* c, void* buff, size_t size) {
+    DeviceGuard g(c->device);
+    uint32_t id = static_cast<uint32_t>(c->windows.size());
+    if (id >= kMaxWindows) throw Error(nimbleInvalidUsage, "register: too many windows");
+    Window w;
+    w.live = buff != nullptr && size > 0;
+    w.base = reinterpret_cast<uint64_t>(buff);
+    w.size = size;
+    if (c->boot) {
+        struct Blob {
+            cudaIpcMemHandle_t h;
+            uint64_t offset, size;
+            int32_t live, pad;
+        } mine{};
+        if (w.live) {
+            auto [base, asz] = allocation_of(buff);
+            (void)asz;
+            CUDA_TRY(cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void*>(base)));
+            mine.offset = w.base - base;
+        }
+        mine.size = size;
+        mine.live = w.live;
+        std::vector<Blob> all(static_cast<size_t>(c->nranks));
+        c->boot->allgather(&mine, sizeof mine, all.data());
+        for (int r = 0; r < c->nranks; ++r) {
+            const Blob& b = all[static_cast<size_t>(r)];
+            uint64_t addr = 0;
+            if (r == c->rank) {
+                addr = w.base;
+            } else if (b.live) {
+                void* p = ipc_cache().acquire(b.h);
+                w.opened.push_back(p);
+                addr = reinterpret_cast<uint64_t>(p) + b.offset;
+            }
+            c->win_table[static_cast<size_t>(id) * kMaxRanks + r] = addr;
+        }
+        CUDA_TRY(cudaMemcpy(c->d_win_table + static_cast<size_t>(id) * kMaxRanks,
+                            &c->win_table[static_cast<size_t>(id) * kMaxRanks], sizeof(uint64_t) * kMaxRanks,
+                            cudaMemcpyHostToDevice));
+    } else {
+        // single process: peers see each other's pointers directly; window k of
+        // every comm in the clique is published as soon as it is registered
+        for (nimbleComm* peer : c->clique->comms) {
+            peer->win_table[static_cast<size_t>(id) * kMaxRanks + c->rank] = w.base;
+            DeviceGuard pg(peer->device);
+            CUDA_TRY(cudaMemcpy(peer->d_win_table + static_cast<size_t>(id) * kMaxRanks + c->rank, &w.base,
+                                sizeof(uint64_t), cudaMemcpyHostToDevice));
+        }
+    }
+    c->windows.push_back(std::move(w));
+    c->view.nwin = static_cast<uint32_t>(c->windows.size());
+    return reinterpret_cast<void*>(static_cast<uintptr_t>(id) + 1);
+}
+
+// ---------------------------------------------------------------- bench
+
+double median(std::vector<double> v) {
+    std::sort(v.begin(), v.end());
+    return v.empty() ? 0.0 : v[v.size() / 2];
+}
+
+void bench_matrix(nimbleComm* c, const std::vector<uint64_t>& m, int warmup, int iters, nimbleBenchResult* out) {
+    if (!c->boot) throw Error(nimbleInvalidUsage, "bench entry points need one process per GPU (nimbleCommInitRank)");
+    if (!out) throw Error(nimbleInvalidArgument, "bench: null result");
+    DeviceGuard g(c->device);
+    const int R = c->nranks, me = c->rank;
+    std::vector<size_t> sc(R), sd(R), rc(R), rd(R);
+    size_t stot = 0, rtot = 0;
+    for (int p = 0; p < R; ++p) {
+        sc[p] = m[static_cast<size_t>(me) * R + p];
+        sd[p] = stot;
+        stot += sc[p];
+        rc[p] = m[static_cast<size_t>(p) * R + me];
+        rd[p] = rtot;
+        rtot += rc[p];
+    }
+    uint8_t *sbuf = nullptr, *rbuf = nullptr;
+    uint64_t* bad = nullptr;
+    CUDA_TRY(cudaMalloc(&sbuf, std::max<size_t>(stot, 16)));
+    CUDA_TRY(cudaMalloc(&rbuf, std::max<size_t>(rtot, 16)));
+    CUDA_TRY(cudaMalloc(&bad, sizeof(uint64_t)));
+    const uint64_t seed = 1;
+    cudaStream_t st = c->bench_stream;
+    for (int p = 0; p < R; ++p) CUDA_TRY(launch_fill(sbuf + sd[p], 0, sc[p], seed, me, p, st));
+    void* handle = register_window(c, rbuf, std::max<size_t>(rtot, 16));
+    (void)handle;
+    auto once = [&] {
+        nimbleResult_t r = nimbleAlltoAllv(sbuf, sc.data(), sd.data(), rbuf, rc.data(), rd.data(), nimbleUint8, c, st);
+        if (r != nimbleSuccess) throw Error(r, g_last_error);
+    };
+    for (int i = 0; i < warmup; ++i) once();
+    CUDA_TRY(cudaStreamSynchronize(st));
+    std::vector<cudaEvent_t> ev(2 * static_cast<size_t>(iters));
+    for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
+    std::vector<double> mine(static_cast<size_t>(iters));
+    for (int i = 0; i < iters; ++i) {
+        c->boot->barrier();
+        CUDA_TRY(cudaEventRecord(ev[2 * i], st));
+        once();
+        CUDA_TRY(cudaEventRecord(ev[2 * i + 1], st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        float ms = 0;
+        CUDA_TRY(cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]));
+        mine[static_cast<size_t>(i)] = ms * 1e-3;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    std::vector<double> all(mine.size() * static_cast<size_t>(R));
+    c->boot->allgather(mine.data(), mine.size() * sizeof(double), all.data());
+    std::vector<double> worst(mine.size(), 0.0);
+    for (int r = 0; r < R; ++r)
+        for (size_t i = 0; i < mine.size(); ++i) worst[i] = std::max(worst[i], all[static_cast<size_t>(r) * mine.size() + i]);
+    // verification pass on a cleared buffer
+    CUDA_TRY(cudaMemsetAsync(rbuf, 0, std::max<size_t>(rtot, 16), st));
+    c->boot->barrier();
+    once();
+    CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(uint64_t), st));
+    for (int p = 0; p < R; ++p) CUDA_TRY(launch_check(rbuf + rd[p], 0, rc[p], seed, p, me, bad, st));
+    uint64_t my_bad = 0;
+    CUDA_TRY(cudaMemcpyAsync(&my_bad, bad, sizeof my_bad, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (c->h_status[0]) throw Error(nimbleRemoteError, "bench: forwarding engine reported async error " +
+                                                           std::to_string(c->h_status[0]));
+    std::vector<uint64_t> bads(static_cast<size_t>(R));
+    c->boot->allgather(&my_bad, sizeof my_bad, bads.data());
+    uint64_t total = 0, worst_port = 0;
+    for (int v = 0; v < R; ++v) {
+        uint64_t eg = 0, ig = 0;
+        for (int p = 0; p < R; ++p) {
+            eg += v == p ? 0 : m[static_cast<size_t>(v) * R + p];
+            ig += v == p ? 0 : m[static_cast<size_t>(p) * R + v];
+            total += m[static_cast<size_t>(v) * R + p];
+        }
+        worst_port = std::max({worst_port, eg, ig});
+    }
+    std::memset(out, 0, sizeof *out);
+    out->seconds_median = median(worst);
+    out->seconds_min = worst.empty() ? 0.0 : *std::min_element(worst.begin(), worst.end());
+    out->total_bytes = total;
+    out->gbps_effective = out->seconds_median > 0 ? static_cast<double>(total) / out->seconds_median / 1e9 : 0.0;
+    out->bound_seconds = static_cast<double>(worst_port) / c->cfg.nvlink_bytes_per_s;
+    for (uint64_t b : bads) out->mismatches += b;
+    {
+        std::vector<uint64_t> mm(m);
+        for (int p = 0; p < R; ++p) mm[static_cast<size_t>(p) * R + p] = 0;
+        const LinkModel lm = comm_model(c);
+        Demand d;
+        d.ranks = R;
+        d.bytes = mm;
+        PlanResult pr = mcf_plan(lm, R, lm.gpus, d, to_params(&c->cfg.planner));
+        out->plan_seconds = pr.stats.wall_seconds;
+        for (const PairRoutes& p : pr.pairs)
+            for (const Flow& f : p.flows) out->relay_flows += p.cands[static_cast<size_t>(f.cand)].via >= 0;
+    }
+    c->boot->barrier();
+    c->windows.back().live = false;
+    for (void* p : c->windows.back().opened) ipc_cache().release(p);
+    c->windows.back().opened.clear();
+    c->schedules.clear();
+    cudaFree(sbuf);
+    cudaFree(rbuf);
+    cudaFree(bad);
+}
+
+}  // namespace
+}  // namespace nb
+
+using nb::fail;
+using nb::guarded;
+
+extern "C" {
+
+nimbleResult_t nimbleCommConfigDefault(nimbleCommConfig* cfg) {
+    if (!cfg) return fail(nimbleInvalidArgument, "config: null");
+    nb::default_config(cfg, 0);
+    return nimbleSuccess;
+}
+
+nimbleResult_t nimbleGetUniqueId(nimbleUniqueId* id) {
+    return guarded([&] {
+        if (!id) throw nb::Error(nimbleInvalidArgument, "null unique id");
+        nb::bootstrap_root(id);
+    });
+}
+
+nimbleResult_t nimbleCommInitRank(nimbleComm_t* out, int nranks, nimbleUniqueId id, int rank) {
+    return guarded([&] {
+        if (!out) throw nb::Error(nimbleInvalidArgument, "null comm");
+        if (nranks < 1 || nranks > nb::kMaxRanks || rank < 0 || rank >= nranks)
+            throw nb::Error(nimbleInvalidArgument, "comm: bad rank / size (max 32 ranks)");
+        auto c = std::make_unique<nimbleComm>();
+        c->rank = rank;
+        c->nranks = nranks;
+        CUDA_TRY(cudaGetDevice(&c->device));
+        nb::default_config(&c->cfg, nranks);
+        c->boot = nb::bootstrap_connect(id, rank, nranks);
+        nb::setup_common(c.get());
+        nb::setup_regions(c.get(), false);
+        nb::upload_view(c.get());
+        c->boot->barrier();
+        *out = c.release();
+    });
+}
+
+nimbleResult_t nimbleCommInitAll(nimbleComm_t* comms, int ndev, const int* devlist) {
+    return guarded([&] {
+        if (!comms || ndev < 1 || ndev > nb::kMaxRanks) throw nb::Error(nimbleInvalidArgument, "comm: bad device list");
+        auto clique = std::make_shared<nb::Clique>();
+        std::vector<std::unique_ptr<nimbleComm>> made;
+        for (int r = 0; r < ndev; ++r) {
+            auto c = std::make_unique<nimbleComm>();
+            c->rank = r;
+            c->nranks = ndev;
+            c->device = devlist ? devlist[r] : r;
+            c->clique = clique;
+            nb::default_config(&c->cfg, ndev);
+            nb::setup_common(c.get());
+            nb::setup_regions(c.get(), true);
+            clique->comms.push_back(c.get());
+            made.push_back(std::move(c));
+        }
+        for (auto& c : made) {
+            nb::DeviceGuard g(c->device);
+            for (auto& p : made) {
+                c->peer_ctrl[static_cast<size_t>(p->rank)] = p->ctrl;
+                c->peer_staging[static_cast<size_t>(p->rank)] = p->staging;
+                if (p->device != c->device) {
+                    cudaError_t e = cudaDeviceEnablePeerAccess(p->device, 0);
+                    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                    else CUDA_TRY(e);
+                }
+            }
+            nb::upload_view(c.get());
+        }
+        for (int r = 0; r < ndev; ++r) comms[r] = made[static_cast<size_t>(r)].release();
+    });
+}
+
+nimbleResult_t nimbleCommDestroy(nimbleComm_t c) {
+    if (!c) return nimbleSuccess;
+    return guarded([&] {
+        {
+            nb::DeviceGuard g(c->device);
+            cudaDeviceSynchronize();
+            if (c->boot) c->boot->barrier();  // nobody touches my regions any more
+            for (nb::Window& w : c->windows)
+                for (void* p : w.opened) nb::ipc_cache().release(p);
+            c->schedules.clear();
+            nb::free_regions(c);
+            cudaFree(c->d_view);
+            cudaFree(c->d_win_table);
+            cudaFree(c->d_scratch);
+            cudaFreeHost(c->h_status);
+            if (c->bench_stream) cudaStreamDestroy(c->bench_stream);
+        }
+        if (c->clique) {
+            auto& v = c->clique->comms;
+            v.erase(std::remove(v.begin(), v.end(), c), v.end());
+        }
+        delete c;
+    });
+}
+
+nimbleResult_t nimbleCommCount(const nimbleComm_t c, int* n) {
+    if (!c || !n) return fail(nimbleInvalidArgument, "null argument");
+    *n = c->nranks;
+    return nimbleSuccess;
+}
+
+nimbleResult_t nimbleCommUserRank(const nimbleComm_t c, int* r) {
+    if (!c || !r) return fail(nimbleInvalidArgument, "null argument");
+    *r = c->rank;
+    return nimbleSuccess;
+}
+
+nimbleResult_t nimbleCommCuDevice(const nimbleComm_t c, int* d) {
+    if (!c || !d) return fail(nimbleInvalidArgument, "null argument");
+    *d = c->device;
+    return nimbleSuccess;
+}
+
+nimbleResult_t nimbleCommGetAsyncError(nimbleComm_t c, nimbleResult_t* err) {
+    if (!c || !err) return fail(nimbleInvalidArgument, "null argument");
+    const uint32_t code = *reinterpret_cast<volatile uint32_t*>(c->h_status);
+    *err = code == 0 ? nimbleSuccess : (code == 5 || code == 6) ? nimbleInvalidUsage : nimbleRemoteError;
+    if (code) {
+        static const char* what[] = {"", "timeout waiting for a receiver's post", "timeout waiting for a staging slot",
+                                     "timeout waiting for a relayed chunk", "timeout waiting for a writer's done flag",
+                                     "send and receive counts disagree across ranks",
+                                     "relay routes need a registered receive buffer",
+                                     "timeout waiting for a relay to drain"};
+        nb::g_last_error = code < 8 ? what[code] : "unknown device error";
+    }
+    return nimbleSuccess;
+}
+
+nimbleResult_t nimbleCommSetConfig(nimbleComm_t c, const nimbleCommConfig* cfg) {
+    return guarded([&] {
+        if (!c || !cfg) throw nb::Error(nimbleInvalidArgument, "null argument");
+        nimbleCommConfig next = *cfg;
+        if (next.gpus_per_node <= 0) next.gpus_per_node = c->nranks;
+        if (next.fabric == nimbleFabricAllToAll && next.gpus_per_node != c->nranks)
+            throw nb::Error(nimbleInvalidArgument, "config: the mesh model must have one GPU per rank");
+        if (!(next.nvlink_bytes_per_s > 0)) throw nb::Error(nimbleInvalidArgument, "config: bandwidth must be positive");
+        nb::slot_count(next);
+        nb::to_params(&next.planner);
+        const bool regrow = next.pipe_chunk != c->cfg.pipe_chunk || next.p2p_buffer != c->cfg.p2p_buffer ||
+                            next.channels_per_peer != c->cfg.channels_per_peer;
+        nb::DeviceGuard g(c->device);
+        if (regrow && c->clique)
+            throw nb::Error(nimbleInvalidUsage, "config: staging geometry is fixed for single-process comms");
+        if (regrow) {
+            CUDA_TRY(cudaDeviceSynchronize());
+            if (c->boot) c->boot->barrier();
+            for (void* p : c->ipc_mapped) cudaIpcCloseMemHandle(p);
+            c->ipc_mapped.clear();
+            cudaFree(c->staging);
+            cudaFree(c->ctrl);
+            c->cfg = next;
+            nb::setup_regions(c, false);
+            nb::upload_view(c);
+            c->epoch = 0;
+        }
+        c->cfg = next;
+        c->plans.clear();
+        c->schedules.clear();
+        if (c->boot) c->boot->barrier();
+    });
+}
+
+nimbleResult_t nimbleCommGetConfig(nimbleComm_t c, nimbleCommConfig* cfg) {
+    if (!c || !cfg) return fail(nimbleInvalidArgument, "null argument");
+    *cfg = c->cfg;
+    return nimbleSuccess;
+}
+
+nimbleResult_t nimbleCommRegister(const nimbleComm_t c, void* buff, size_t size, void** handle) {
+    return guarded([&] {
+        if (!c || !handle) throw nb::Error(nimbleInvalidArgument, "null argument");
+        *handle = nb::register_window(c, buff, size);
+        nb::upload_view(c);
+    });
+}
+
+nimbleResult_t nimbleCommDeregister(const nimbleComm_t c, void* handle) {
+    return guarded([&] {
+        if (!c) throw nb::Error(nimbleInvalidArgument, "null comm");
+        const size_t id = reinterpret_cast<uintptr_t>(handle) - 1;
+        if (id >= c->windows.size() || !c->windows[id].live) throw nb::Error(nimbleInvalidArgument, "bad handle");
+        nb::DeviceGuard g(c->device);
+        CUDA_TRY(cudaDeviceSynchronize());
+        if (c->boot) c->boot->barrier();
+        for (void* p : c->windows[id].opened) nb::ipc_cache().release(p);
+        c->windows[id].opened.clear();
+        c->windows[id].live = false;
+        c->schedules.clear();
+    });
+}
+
+nimbleResult_t nimbleMemAlloc(void** ptr, size_t size) {
+    return guarded([&] {
+        if (!ptr) throw nb::Error(nimbleInvalidArgument, "null pointer");
+        CUDA_TRY(cudaMalloc(ptr, std::max<size_t>(size, 16)));
+    });
+}
+
+nimbleResult_t nimbleMemFree(void* ptr) {
+    return guarded([&] { CUDA_TRY(cudaFree(ptr)); });
+}
+
+nimbleResult_t nimbleGroupStart(void) {
+    ++nb::g_group_depth;
+    return nimbleSuccess;
+}
+
+nimbleResult_t nimbleGroupEnd(void) {
+    if (nb::g_group_depth <= 0) return fail(nimbleInvalidUsage, "group end without start");
+    if (--nb::g_group_depth > 0) return nimbleSuccess;
+    return guarded([&] { nb::flush_group(); });
+}
+
+nimbleResult_t nimbleSend(const void* sendbuff, size_t count, nimbleDataType_t dt, int peer, nimbleComm_t comm,
+                          void* stream) {
+    return guarded([&] {
+        if (!comm || peer < 0 || peer >= comm->nranks) throw nb::Error(nimbleInvalidArgument, "send: bad peer");
+        nb::PendingOp op{nb::PendingOp::Send, comm, static_cast<cudaStream_t>(stream), peer,
+                         reinterpret_cast<uint64_t>(sendbuff), count * nb::elem_size(dt), 0, 0, {}, {}, {}, {}};
+        nimbleResult_t r = nb::enqueue(std::move(op));
+        if (r != nimbleSuccess) throw nb::Error(r, nb::g_last_error);
+    });
+}
+
+nimbleResult_t nimbleRecv(void* recvbuff, size_t count, nimbleDataType_t dt, int peer, nimbleComm_t comm, void* stream) {
+    return guarded([&] {
+        if (!comm || peer < 0 || peer >= comm->nranks) throw nb::Error(nimbleInvalidArgument, "recv: bad peer");
+        nb::PendingOp op{nb::PendingOp::Recv, comm, static_cast<cudaStream_t>(stream), peer,
+                         reinterpret_cast<uint64_t>(recvbuff), count * nb::elem_size(dt), 0, 0, {}, {}, {}, {}};
+        nimbleResult_t r = nb::enqueue(std::move(op));
+        if (r != nimbleSuccess) throw nb::Error(r, nb::g_last_error);
+    });
+}
+
+nimbleResult_t nimbleAlltoAllv(const void* sendbuff, const size_t sendcounts[], const size_t sdispls[], void* recvbuff,
+                               const size_t recvcounts[], const size_t rdispls[], nimbleDataType_t dt,
+                               nimbleComm_t comm, void* stream) {
+    return guarded([&] {
+        if (!comm || !sendcounts || !sdispls || !recvcounts || !rdispls)
+            throw nb::Error(nimbleInvalidArgument, "alltoallv: null argument");
+        const size_t es = nb::elem_size(dt);
+        nb::PendingOp op{nb::PendingOp::AllToAllV, comm, static_cast<cudaStream_t>(stream), -1, 0, 0,
+                         reinterpret_cast<uint64_t>(sendbuff), reinterpret_cast<uint64_t>(recvbuff), {}, {}, {}, {}};
+        for (int p = 0; p < comm->nranks; ++p) {
+            op.sbytes.push_back(sendcounts[p] * es);
+            op.soff.push_back(sdispls[p] * es);
+            op.rbytes.push_back(recvcounts[p] * es);
+            op.roff.push_back(rdispls[p] * es);
+        }
+        nimbleResult_t r = nb::enqueue(std::move(op));
+        if (r != nimbleSuccess) throw nb::Error(r, nb::g_last_error);
+    });
+}
+
+nimbleResult_t nimbleAlltoAll(const void* sendbuff, void* recvbuff, size_t count, nimbleDataType_t dt,
+                              nimbleComm_t comm, void* stream) {
+    if (!comm) return fail(nimbleInvalidArgument, "alltoall: null comm");
+    std::vector<size_t> counts(static_cast<size_t>(comm->nranks), count), displs(static_cast<size_t>(comm->nranks));
+    for (int p = 0; p < comm->nranks; ++p) displs[static_cast<size_t>(p)] = count * static_cast<size_t>(p);
+    return nimbleAlltoAllv(sendbuff, counts.data(), displs.data(), recvbuff, counts.data(), displs.data(), dt, comm,
+                           stream);
+}
+
+nimbleResult_t nimbleFillPayload(void* buf, uint64_t first, uint64_t n, uint64_t seed, int s, int d, void* stream) {
+    return guarded([&] { CUDA_TRY(nb::launch_fill(buf, first, n, seed, s, d, static_cast<cudaStream_t>(stream))); });
+}
+
+nimbleResult_t nimbleCheckPayload(const void* buf, uint64_t first, uint64_t n, uint64_t seed, int s, int d,
+                                  uint64_t* bad, void* stream) {
+    return guarded([&] {
+        CUDA_TRY(nb::launch_check(buf, first, n, seed, s, d, bad, static_cast<cudaStream_t>(stream)));
+    });
+}
+
+nimbleResult_t nimbleBenchMatrix(nimbleComm_t c, const uint64_t* matrix, int warmup, int iters,
+                                 nimbleBenchResult* out) {
+    return guarded([&] {
+        if (!c || !matrix || iters < 1 || warmup < 0) throw nb::Error(nimbleInvalidArgument, "bench: bad argument");
+        std::vector<uint64_t> m(matrix, matrix + static_cast<size_t>(c->nranks) * c->nranks);
+        nb::bench_matrix(c, m, warmup, iters, out);
+    });
+}
+
+nimbleResult_t nimbleBenchP2P(nimbleComm_t c, uint64_t bytes, int src, int dst, int warmup, int iters,
+                              nimbleBenchResult* out) {
+    return guarded([&] {
+        if (!c) throw nb::Error(nimbleInvalidArgument, "bench: null comm");
+        nb::Demand d = nb::demand_p2p(c->nranks, src, dst, bytes);
+        nb::bench_matrix(c, d.bytes, warmup, iters, out);
+    });
+}
+
+nimbleResult_t nimbleBenchSkewed(nimbleComm_t c, uint64_t per_rank, double ratio, int hot, int warmup, int iters,
+                                 nimbleBenchResult* out) {
+    return guarded([&] {
+        if (!c) throw nb::Error(nimbleInvalidArgument, "bench: null comm");
+        nb::Demand d = nb::demand_skewed(c->nranks, per_rank, ratio, hot, false);
+        nb::bench_matrix(c, d.bytes, warmup, iters, out);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,113 @@
+// Plain-old-data shared by the host runtime and the sm_100a forwarding engine.
+//
+// Per rank the comm owns two IPC-exported device regions:
+//   ctrl    : Ctrl header (receive posts + done flags) followed by the ready
+//             flags of the staging rings hosted here and the consumed flags of
+//             the rings this rank feeds;
+//   staging : one ring of `slots` x `pipe_chunk` bytes per ordered pair (s,d)
+//             hosted on this rank (used when this rank relays s->d, or, for
+//             s->me, when my receive buffer is not registered).
+// The flag protocol is the reference's bounded-buffer recurrence
+// (proj/src/pipeline.cpp:97-106): chunk k of a
+// ring may enter the staging slot k % S only after the forwarder has drained
+// chunk k - S (consumed flag), and may leave it only after it has landed
+// (ready flag).  Flags carry (epoch << 32 | k + 1) tags, so no reset is needed
+// between calls.
+#pragma once
+
+#if !defined(__CUDACC__) && !defined(__host__)
+#define __host__
+#define __device__
+#endif
+
+#include <cstdint>
+
+namespace nb {
+
+constexpr int kMaxRanks = 32;
+constexpr int kMaxSlots = 64;
+constexpr int kThreads = 512;  // forwarding-engine CTA size
+
+enum ItemKind : uint8_t {
+    kLocal = 0,    // src -> dst, both local absolute addresses
+    kPush = 1,     // my send range -> receiver `peer` (zero copy, or its self ring when staged)
+    kStage = 2,    // my send range -> ring (me, aux) hosted on relay `peer`
+    kForward = 3,  // ring (aux, peer) hosted here -> receiver `peer` (or my own buffer)
+};
+
+// One unit of the chunk schedule, 32 bytes.
+struct Item {
+    uint64_t src;    // kLocal/kPush/kStage: absolute local source address
+    uint64_t dst;    // kLocal: absolute; kPush/kForward: byte offset inside the pair segment
+    uint32_t bytes;  // <= pipe_chunk for ring traffic
+    uint8_t kind;
+    uint8_t peer;    // kLocal: unused; kPush: receiver; kStage: relay; kForward: final receiver
+    uint16_t aux;    // kStage: final receiver; kForward: original sender
+    uint32_t seq;    // chunk index in the ring / flow
+    uint32_t pad;
+};
+static_assert(sizeof(Item) == 32, "Item layout");
+
+enum PostMode : uint32_t { kPostZeroCopy = 1, kPostStaged = 2 };
+
+// Receiver d publishes, for each sender s, where s's segment lands.
+struct Post {
+    uint64_t tag;    // epoch of the call this post belongs to
+    uint32_t win;    // registered window id (zero copy)
+    uint32_t mode;   // PostMode
+    uint64_t off;    // byte offset of the pair segment inside the window
+    uint64_t bytes;  // expected byte count (checked against the sender's)
+};
+static_assert(sizeof(Post) == 32, "Post layout");
+
+struct CtrlHeader {
+    Post post[kMaxRanks];       // written by me (the receiver), read by writers
+    uint64_t done[kMaxRanks];   // done[w] = epoch: writer w finished writing into me
+};
+
+// Geometry of the flag arrays that follow the header inside ctrl.
+struct FlagLayout {
+    static constexpr uint64_t header = (sizeof(CtrlHeader) + 255) / 256 * 256;
+    // ready flags of ring (s, d) hosted here: [s][d][slot]
+    __host__ __device__ static constexpr uint64_t ready_off(int R, int s, int d, int slot) {
+        return header + 8ull * ((static_cast<uint64_t>(s) * R + d) * kMaxSlots + slot);
+    }
+    // consumed flags of ring (me, d) hosted on relay v: [d][v][slot]
+    __host__ __device__ static constexpr uint64_t consumed_off(int R, int d, int v, int slot) {
+        return header + 8ull * static_cast<uint64_t>(R) * R * kMaxSlots +
+               8ull * ((static_cast<uint64_t>(d) * R + v) * kMaxSlots + slot);
+    }
+    __host__ __device__ static constexpr uint64_t bytes(int R) { return header + 16ull * R * R * kMaxSlots; }
+};
+
+// Comm-lifetime device view (set up once at init / registration).
+struct CommDevice {
+    int rank, nranks;
+    uint8_t* ctrl[kMaxRanks];     // ctrl region of every rank, mapped here
+    uint8_t* staging[kMaxRanks];  // staging region of every rank, mapped here
+    uint64_t* win_table;          // [win * kMaxRanks + rank] -> mapped window base
+    uint32_t nwin;
+    uint32_t timeout_ms;
+    uint32_t* status;             // host-mapped: [0] error code, [1] detail
+    uint32_t* scratch;            // [0] queue head, [1] CTAs done, [2..2+R) push counters
+};
+
+// Per-launch arguments (passed by value as a __grid_constant__ kernel parameter).
+struct LaunchArgs {
+    const Item* items;
+    uint32_t nitems;
+    uint32_t slots;        // S
+    uint64_t pipe_chunk;   // ring slot bytes
+    uint64_t epoch;
+    const CommDevice* comm;
+    const Post* posts;     // [R] my receive posts for this call (device copy)
+    uint32_t push_items[kMaxRanks];   // kPush items to receiver d (count toward done if zero copy)
+    uint32_t fwd_items[kMaxRanks];    // kForward items into receiver d != me
+    uint64_t expect_done;             // bitmask of writers I must hear `done` from
+    uint64_t send_bytes[kMaxRanks];   // my outgoing pair sizes (checked against receivers' posts)
+    const uint64_t* final_waits;      // pairs (ctrl byte offset of consumed flag, chunk index)
+    uint32_t nfinal;
+    uint32_t local_only;              // 1: flagless single-GPU exchange (no ctrl)
+};
+
+}  // namespace nb

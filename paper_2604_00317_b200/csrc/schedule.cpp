@@ -1,0 +1,169 @@
+// Chunk scheduler; see schedule.hpp.
+#include "schedule.hpp"
+
+#include <algorithm>
+#include <stdexcept>
+
+#include "capi_util.hpp"
+
+namespace nb {
+
+namespace {
+
+struct Keyed {
+    double key;
+    uint64_t flow_bytes;
+    uint32_t order;  // insertion order: deterministic tie break
+    Item item;
+};
+
+void cut(std::vector<Keyed>& out, Item proto, uint64_t src0, uint64_t dst0, uint64_t bytes, uint64_t chunk,
+         double phase) {
+    const uint64_t n = (bytes + chunk - 1) / chunk;
+    for (uint64_t k = 0; k < n; ++k) {
+        Item it = proto;
+        const uint64_t off = k * chunk;
+        it.src = src0 ? src0 + off : 0;
+        it.dst = dst0 + off;
+        it.bytes = static_cast<uint32_t>(std::min(chunk, bytes - off));
+        it.seq = static_cast<uint32_t>(k);
+        out.push_back({(static_cast<double>(k) + 0.5) / static_cast<double>(n) + phase, bytes,
+                       static_cast<uint32_t>(out.size()), it});
+    }
+}
+
+std::vector<Item> ordered(std::vector<Keyed>& v) {
+    std::sort(v.begin(), v.end(), [](const Keyed& a, const Keyed& b) {
+        if (a.key != b.key) return a.key < b.key;
+        if (a.flow_bytes != b.flow_bytes) return a.flow_bytes > b.flow_bytes;  // hot flows first on ties
+        return a.order < b.order;
+    });
+    std::vector<Item> items;
+    items.reserve(v.size());
+    for (const Keyed& k : v) items.push_back(k.item);
+    return items;
+}
+
+constexpr double kHop2 = 1e-9;  // forward of chunk k sorts right after its stage-in
+
+}  // namespace
+
+Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t pipe_chunk, uint32_t slots,
+                        uint64_t local_chunk) {
+    const int R = rb.R, me = rb.me;
+    if (R > kMaxRanks) throw Error(nimbleInvalidArgument, "schedule: too many ranks");
+    if (pipe_chunk == 0 || pipe_chunk > 0xffffffffull) throw Error(nimbleInvalidArgument, "schedule: bad pipe_chunk");
+    if (slots == 0 || slots > kMaxSlots) throw Error(nimbleInvalidArgument, "schedule: bad slot count");
+    Schedule sc;
+    sc.posts = rb.recv_post;
+    std::vector<Keyed> keyed;
+
+    // self segment: local copy
+    if (rb.send_bytes[me] != rb.recv_bytes[me])
+        throw Error(nimbleInvalidArgument, "alltoallv: self send and receive counts differ");
+    if (rb.send_bytes[me]) {
+        Item proto{};
+        proto.kind = kLocal;
+        proto.peer = static_cast<uint8_t>(me);
+        cut(keyed, proto, rb.send_ptr[me], rb.recv_ptr[me], rb.send_bytes[me], std::max<uint64_t>(local_chunk, 1), 0.0);
+        sc.moved_bytes += rb.send_bytes[me];
+    }
+
+    for (const PairRoutes& pr : plan.pairs) {
+        const int s = pr.src, d = pr.dst;
+        if (s != me && d != me) {
+            // only relay duty can involve me
+            bool relays_me = false;
+            for (const Flow& f : pr.flows)
+                relays_me |= pr.cands[static_cast<size_t>(f.cand)].via == me;
+            if (!relays_me) continue;
+        }
+        if (s == me && pr.demand != rb.send_bytes[d])
+            throw Error(nimbleInvalidArgument, "schedule: plan demand differs from the send count");
+        if (d == me && pr.demand != rb.recv_bytes[s])
+            throw Error(nimbleInvalidArgument, "alltoallv: receive count differs from the planned demand");
+        uint64_t off = 0;
+        for (const Flow& f : pr.flows) {
+            const Candidate& c = pr.cands[static_cast<size_t>(f.cand)];
+            const uint64_t bytes = static_cast<uint64_t>(f.bytes);
+            if (static_cast<double>(bytes) != f.bytes) throw Error(nimbleInternalError, "schedule: fractional flow");
+            if (c.route == Route::Rail) throw Error(nimbleInvalidUsage, "schedule: inter-node rail routes need a multi-node box");
+            if (c.route == Route::Direct) {
+                if (s == me) {
+                    Item proto{};
+                    proto.kind = kPush;
+                    proto.peer = static_cast<uint8_t>(d);
+                    const size_t first = keyed.size();
+                    cut(keyed, proto, rb.send_ptr[d] + off, off, bytes, pipe_chunk, 0.0);
+                    sc.push_items[d] += static_cast<uint32_t>(keyed.size() - first);
+                    sc.moved_bytes += bytes;
+                }
+                if (d == me) {
+                    if (rb.recv_post[s].mode == kPostStaged) {  // drain my self ring (s, me)
+                        Item proto{};
+                        proto.kind = kForward;
+                        proto.peer = static_cast<uint8_t>(me);
+                        proto.aux = static_cast<uint16_t>(s);
+                        cut(keyed, proto, 0, off, bytes, pipe_chunk, kHop2);
+                    } else {
+                        sc.expect_done |= 1ull << s;
+                    }
+                }
+            } else {  // two-hop relay through GPU `via`
+                const int v = c.via;
+                if (v < 0 || v >= R) throw Error(nimbleInvalidUsage, "schedule: relay GPU is not a rank of this comm");
+                if (s == me) {
+                    ++sc.relay_flows;
+                    Item proto{};
+                    proto.kind = kStage;
+                    proto.peer = static_cast<uint8_t>(v);
+                    proto.aux = static_cast<uint16_t>(d);
+                    cut(keyed, proto, rb.send_ptr[d] + off, off, bytes, pipe_chunk, 0.0);
+                    sc.moved_bytes += bytes;
+                    // before returning, the last chunk of every used slot must be drained
+                    const uint64_t n = (bytes + pipe_chunk - 1) / pipe_chunk;
+                    for (uint64_t k = n > slots ? n - slots : 0; k < n; ++k) {
+                        sc.final_waits.push_back(FlagLayout::consumed_off(R, d, v, static_cast<int>(k % slots)));
+                        sc.final_waits.push_back(k);
+                    }
+                }
+                if (v == me) {
+                    Item proto{};
+                    proto.kind = kForward;
+                    proto.peer = static_cast<uint8_t>(d);
+                    proto.aux = static_cast<uint16_t>(s);
+                    const size_t first = keyed.size();
+                    cut(keyed, proto, 0, off, bytes, pipe_chunk, kHop2);
+                    sc.fwd_items[d] += static_cast<uint32_t>(keyed.size() - first);
+                }
+                if (d == me) sc.expect_done |= 1ull << v;
+            }
+            off += bytes;
+        }
+    }
+    sc.items = ordered(keyed);
+    return sc;
+}
+
+std::vector<Item> build_local_items(int R, const uint64_t* m, const uint64_t* send_base, const uint64_t* recv_base,
+                                    uint64_t chunk) {
+    std::vector<Keyed> keyed;
+    for (int s = 0; s < R; ++s) {
+        uint64_t soff = 0;
+        for (int d = 0; d < R; ++d) {
+            const uint64_t b = m[static_cast<size_t>(s) * R + d];
+            if (b) {
+                uint64_t roff = 0;
+                for (int x = 0; x < s; ++x) roff += m[static_cast<size_t>(x) * R + d];
+                Item proto{};
+                proto.kind = kLocal;
+                proto.peer = static_cast<uint8_t>(d);
+                cut(keyed, proto, send_base[s] + soff, recv_base[d] + roff, b, chunk, 0.0);
+            }
+            soff += b;
+        }
+    }
+    return ordered(keyed);
+}
+
+}  // namespace nb

@@ -1,0 +1,50 @@
+// The chunk scheduler: turns the replicated plan plus this rank's buffers into
+// the rank's ordered work-item list for the forwarding engine.
+//
+// Byte-range convention (the reference defines
+// none): a pair's flows, in candidate order (direct first, then relays in
+// ascending GPU order), take consecutive ranges of the pair segment; every
+// ring-borne flow is cut into pipe_chunk units with a short tail
+// (proj/src/pipeline.cpp:85-91), chunk k riding staging slot k % S.
+//
+// Order: each item gets the key (k + 0.5) / n of its flow (progress fraction)
+// plus a tiny phase offset for hop 2, so all flows advance in proportion and
+// finish together (the hot destination's port is fed from t = 0 to the end),
+// and every cross-rank wait points at a strictly smaller key -- the engine's
+// deadlock-freedom argument (engine.cu).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "device.cuh"
+#include "planner.hpp"
+
+namespace nb {
+
+struct RankBuffers {
+    int R = 0, me = 0;
+    std::vector<uint64_t> send_ptr, send_bytes;  // [R] my outgoing segments
+    std::vector<uint64_t> recv_ptr, recv_bytes;  // [R] my incoming segments
+    std::vector<Post> recv_post;                 // [R] mode/win/off per sender (tag != 0: present)
+};
+
+struct Schedule {
+    std::vector<Item> items;
+    std::vector<Post> posts;
+    std::vector<uint64_t> final_waits;  // (ctrl byte offset, chunk index) pairs
+    uint32_t push_items[kMaxRanks] = {};
+    uint32_t fwd_items[kMaxRanks] = {};
+    uint64_t expect_done = 0;
+    int relay_flows = 0;
+    uint64_t moved_bytes = 0;  // my outgoing payload (incl. self segment)
+};
+
+Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t pipe_chunk, uint32_t slots,
+                        uint64_t local_chunk);
+
+// 1-GPU emulated exchange: every pair's segment as local copies (packed layout).
+std::vector<Item> build_local_items(int R, const uint64_t* matrix, const uint64_t* send_base,
+                                    const uint64_t* recv_base, uint64_t chunk);
+
+}  // namespace nb
