@@ -1,0 +1,495 @@
+#!/usr/bin/env python
+"""bench.py -- skewed all-to-allv through the B200 forwarding engine.
+
+Default (no torchrun, N=1): BASELINE config c3 -- skewed all-to-allv, 8 ranks,
+256 MiB per rank, hotspot ratio 0.7 -- with all 8 ranks' buffers on one GPU,
+moved by ONE forwarding-engine launch per step (nimbleExchangeLocal): the
+1-GPU local-copy calibration of the data path (north star: "1 GPU for
+local-copy calibration").  Bound: HBM (read + write of every payload byte).
+
+Under torchrun (N > 1): one process per GPU, the same workload on R = N real
+ranks over NVLink (nimbleAlltoAllv, registered receive buffers, zero copy),
+NCCL all-to-allv on the same buffers beside it.  Bound: the MCF port bound,
+max over GPUs of egress/ingress bytes / 900 GB/s.
+
+--impl reference: the reference's CPU path on the host cores -- its own
+plan() (oracle/_ref, compiled from /root/reference) followed by the CPU
+restatement of the delivery (oracle/cpu_exchange.c, all threads).  The
+reference itself moves no bytes.
+
+One JSON line on rank 0.  Timing: W untimed warm-up steps, K timed steps
+between barrier + cuda.synchronize, CUDA events on the launching stream, max
+over ranks.  Inputs (2 GiB at N=1, >= 256 MiB per rank at N>1) exceed the
+126 MB L2, so no flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "skewed all-to-allv effective GB/s vs hotspot ratio at 8 GPUs; p2p relay GB/s"
+MiB = 1 << 20
+PORT_GBPS = 900.0  # NVLink-5 port, per direction per GPU (north star roofline)
+
+
+# ------------------------------------------------------------------ helpers
+
+def workload_matrix(R, per_rank, ratio, hot=0):
+    """gen_skewed_a2av(R, per_rank, ratio, hot) through the product C ABI."""
+    from paper_2604_00317_b200 import planner as P
+    return P.gen_skewed_a2av(R, per_rank, ratio, hot)
+
+
+def max_over_ranks(x: float) -> float:
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return x
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier():
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+
+
+def port_bytes(m, R):
+    worst = 0
+    for v in range(R):
+        worst = max(worst, sum(m[v * R + d] for d in range(R) if d != v),
+                    sum(m[s * R + v] for s in range(R) if s != v))
+    return worst
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.reader = threading.Thread(target=self._read, daemon=True)
+            self.reader.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(R, m, max_seconds=20.0):
+    """The reference's CPU path on the host: reference plan() + CPU delivery.
+
+    Test infrastructure (oracle/) -- the checker side, timed as the baseline.
+    Returns (GB/s, cores, kind, sample, model_gbps)."""
+    import numpy as np
+    from oracle import ref
+    cores = os.cpu_count() or 1
+    cpu = ref.cpu_lib()
+    req = {"ranks": R, "topology": {"nodes": 1, "gpus": R, "nics": 0, "fabric": "nvswitch",
+                                    "nvlink_gbps": PORT_GBPS, "rail_gbps": 50.0},
+           "workload": {"kind": "matrix", "bytes": list(m)}}
+    kind = "reference" if ref.available() else "port"
+    model = None
+    if kind == "reference":
+        src, dst, via, byt = ref.plan_flows(req)
+        model = ref.call(dict(req, op="simulate"))["model_gbps"]
+    else:
+        from oracle import nimble_oracle as O
+        t = O.build_canonical(1, R, 0, PORT_GBPS * 1e9, 0, O.NVSWITCH)
+        p = O.plan(t, R, R, m)
+        src, dst, via, byt = [], [], [], []
+        for pp in p.pairs:
+            for c, b in pp.flows:
+                src.append(pp.src), dst.append(pp.dst), via.append(pp.candidates[c].via), byt.append(b)
+    rows = [sum(m[s * R:(s + 1) * R]) for s in range(R)]
+    cols = [sum(m[x * R + d] for x in range(R)) for d in range(R)]
+    send = [np.ones(max(r, 1), dtype=np.uint8) for r in rows]
+    recv = [np.zeros(max(c, 1), dtype=np.uint8) for c in cols]
+    mat = (ctypes.c_uint64 * (R * R))(*m)
+    sp = (ctypes.c_void_p * R)(*[a.ctypes.data for a in send])
+    rp = (ctypes.c_void_p * R)(*[a.ctypes.data for a in recv])
+    n = len(src)
+    arr = lambda t, v: (t * max(n, 1))(*v)  # noqa: E731
+    total = sum(m)
+    reps, spent = 0, 0.0
+    while reps < 1 or (spent < max_seconds and reps < 20):
+        t0 = time.perf_counter()
+        if kind == "reference":
+            ref.time_plan(req, 0, 1)  # the reference's plan() on this matrix
+        cpu.orc_exchange_flows(R, mat, sp, rp, n, arr(ctypes.c_int, src), arr(ctypes.c_int, dst),
+                               arr(ctypes.c_int, via), arr(ctypes.c_double, byt), None, 1 << 20, cores)
+        spent += time.perf_counter() - t0
+        reps += 1
+    sample = (f"{reps} x full matrix ({total / 2**30:.2f} GiB, R={R}): reference plan() + "
+              f"host memcpy delivery on {cores} threads")
+    return total * reps / spent / 1e9, cores, kind, sample, model
+
+
+# ------------------------------------------------------------------ N = 1
+
+def run_local(args):
+    import torch
+    from paper_2604_00317_b200 import comm as C
+    torch.cuda.set_device(0)
+    R, per_rank, ratio = 8, args.per_rank_mib * MiB, args.ratio
+    m = workload_matrix(R, per_rank, ratio)
+    total = sum(m)
+    rows = [sum(m[s * R:(s + 1) * R]) for s in range(R)]
+    cols = [sum(m[x * R + d] for x in range(R)) for d in range(R)]
+    sends = [torch.empty(max(r, 16), dtype=torch.uint8, device="cuda") for r in rows]
+    recvs = [torch.zeros(max(c, 16), dtype=torch.uint8, device="cuda") for c in cols]
+    for s in range(R):
+        sc, sd, _, _ = C.packed_displs(m, R, s)
+        for d in range(R):
+            C.fill_payload(sends[s][sd[d]:], 0, sc[d], 1, s, d)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        C.exchange_local(sends, recvs, m, args.ctas, stream)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with Clocks(0) as clk:
+        torch.cuda.synchronize()
+        ev[0].record(stream)
+        for k in range(args.steps):
+            C.exchange_local(sends, recvs, m, args.ctas, stream)
+            ev[k + 1].record(stream)
+        torch.cuda.synchronize()
+    per_step = [ev[k].elapsed_time(ev[k + 1]) * 1e-3 for k in range(args.steps)]
+    t_total = ev[0].elapsed_time(ev[-1]) * 1e-3
+    # verify the last step's delivery
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for d in range(R):
+        _, _, rc, rd = C.packed_displs(m, R, d)
+        for s in range(R):
+            C.check_payload(recvs[d][rd[s]:], 0, rc[s], 1, s, d, bad)
+    mismatches = int(bad.item())
+
+    # torch D2D copies of the same segments (library baseline on one GPU)
+    torch_gbps = None
+    if not args.no_baselines:
+        segs = []
+        for s in range(R):
+            sc, sd, _, _ = C.packed_displs(m, R, s)
+            for d in range(R):
+                _, _, _, rd = C.packed_displs(m, R, d)
+                if sc[d]:
+                    segs.append((recvs[d][rd[s]:rd[s] + sc[d]], sends[s][sd[d]:sd[d] + sc[d]]))
+        for _ in range(2):
+            for dst, src in segs:
+                dst.copy_(src)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            for dst, src in segs:
+                dst.copy_(src)
+        e1.record()
+        torch.cuda.synchronize()
+        torch_gbps = total * args.steps / (e0.elapsed_time(e1) * 1e-3) / 1e9
+
+    # end to end through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        hs = [torch.empty(t.numel(), dtype=torch.uint8, pin_memory=True) for t in sends]
+        hr = [torch.empty(t.numel(), dtype=torch.uint8, pin_memory=True) for t in recvs]
+        for h, t in zip(hs, sends):
+            h.copy_(t)
+        ksteps = max(3, min(args.steps, 10))
+
+        def e2e_step():
+            for h, t in zip(hs, sends):
+                t.copy_(h, non_blocking=True)
+            C.exchange_local(sends, recvs, m, args.ctas, stream)
+            for h, t in zip(hr, recvs):
+                h.copy_(t, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ksteps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = e0.elapsed_time(e1) * 1e-3 / ksteps
+        e2e = {"value": total / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": sum(t.numel() for t in sends),
+               "d2h_bytes_per_step": sum(t.numel() for t in recvs), "steps": ksteps}
+
+    peak, peak_src = measured_peaks()
+    kernel_s = sum(per_step) / len(per_step)
+    achieved = 2 * total / kernel_s / 1e9
+    line = {
+        "metric": METRIC, "value": total * args.steps / t_total / 1e9, "unit": "GB/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_total / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic: gen_skewed_a2av matrix, splitmix64 payload bytes (seed 1)",
+        "config": {"workload": f"c3 skewed all-to-allv, {R} ranks emulated on 1 GPU (local-copy calibration), "
+                               f"{args.per_rank_mib} MiB/rank, hotspot ratio {ratio}, hot rank 0",
+                   "ranks": R, "per_rank_bytes": per_rank, "ratio": ratio, "total_bytes": total,
+                   "layout": "packed MPI all-to-allv (misaligned segments)",
+                   "l2": f"inputs {total / 2**30:.2f} GiB > 126 MB L2, no flush"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": _ncu_traffic("local"),
+                     "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)",
+                     "algorithmic_bytes_per_launch": 2 * total, "kernel": "nb::exchange_kernel"},
+        "verified": {"mismatched_bytes": mismatches},
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "baselines": {"torch_copy_gbps": torch_gbps},
+    }
+    if not args.no_cpu:
+        v, cores, kind, sample, model = cpu_baseline(R, m, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": v, "unit": "GB/s", "cores": cores, "kind": kind, "sample": sample,
+                                "reference_model_gbps": model}
+    if mismatches:
+        line["error"] = f"delivery mismatch: {mismatches} bytes"
+    return line
+
+
+def _ncu_traffic(tag):
+    """dram read+write bytes per launch from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(tag)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ N > 1
+
+def run_multi(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2604_00317_b200 import comm as C
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    uid = [C.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, 0)
+    comm = C.Comm.init_rank(world, uid[0], rank)
+    R = world
+    per_rank, ratio = args.per_rank_mib * MiB, args.ratio
+    m = workload_matrix(R, per_rank, ratio)
+    total = sum(m)
+    sc, sd, rc, rd = C.packed_displs(m, R, rank)
+    send = torch.empty(max(sum(sc), 16), dtype=torch.uint8, device="cuda")
+    recv = torch.zeros(max(sum(rc), 16), dtype=torch.uint8, device="cuda")
+    for d in range(R):
+        C.fill_payload(send[sd[d]:], 0, sc[d], 1, rank, d)
+    handle = comm.register(recv)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        comm.alltoallv(send, sc, sd, recv, rc, rd, stream)
+    torch.cuda.synchronize()
+    comm.check_async()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            comm.alltoallv(send, sc, sd, recv, rc, rd, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    t = max_over_ranks(e0.elapsed_time(e1) * 1e-3)
+    comm.check_async()
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for s in range(R):
+        C.check_payload(recv[rd[s]:], 0, rc[s], 1, s, rank, bad)
+    torch.cuda.synchronize()
+    mismatches = int(max_over_ranks(float(bad.item())))
+
+    nccl = None
+    if not args.no_baselines:
+        pg = dist.new_group(backend="nccl")
+        out = torch.empty_like(recv)
+        ins, outs = list(sc), list(rc)
+        sview, rview = send[:sum(sc)], out[:sum(rc)]
+        for _ in range(args.warmup):
+            dist.all_to_all_single(rview, sview, outs, ins, group=pg)
+        torch.cuda.synchronize()
+        barrier()
+        n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n0.record()
+        for _ in range(args.steps):
+            dist.all_to_all_single(rview, sview, outs, ins, group=pg)
+        n1.record()
+        torch.cuda.synchronize()
+        tn = max_over_ranks(n0.elapsed_time(n1) * 1e-3)
+        nccl = {"value": total * args.steps / tn / 1e9, "ms_per_step": tn / args.steps * 1e3,
+                "call": "torch.distributed.all_to_all_single (NCCL)"}
+
+    e2e = None
+    if not args.no_e2e:
+        hs = torch.empty(send.numel(), dtype=torch.uint8, pin_memory=True)
+        hr = torch.empty(recv.numel(), dtype=torch.uint8, pin_memory=True)
+        hs.copy_(send)
+        ksteps = max(3, min(args.steps, 10))
+
+        def e2e_step():
+            send.copy_(hs, non_blocking=True)
+            comm.alltoallv(send, sc, sd, recv, rc, rd, stream)
+            hr.copy_(recv, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(ksteps):
+            e2e_step()
+        a1.record(stream)
+        torch.cuda.synchronize()
+        te = max_over_ranks(a0.elapsed_time(a1) * 1e-3) / ksteps
+        e2e = {"value": total / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": send.numel() * R,
+               "d2h_bytes_per_step": recv.numel() * R, "steps": ksteps, "note": "bytes summed over ranks"}
+
+    comm.deregister(handle)
+    bound_s = port_bytes(m, R) / (PORT_GBPS * 1e9)
+    step_s = t / args.steps
+    achieved = port_bytes(m, R) / step_s / 1e9
+    line = {
+        "metric": METRIC, "value": total * args.steps / t / 1e9, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic: gen_skewed_a2av matrix, splitmix64 payload bytes (seed 1)",
+        "config": {"workload": f"skewed all-to-allv, {R} ranks (1 per GPU, NVLink), {args.per_rank_mib} MiB/rank, "
+                               f"hotspot ratio {ratio}, hot rank 0",
+                   "ranks": R, "per_rank_bytes": per_rank, "ratio": ratio, "total_bytes": total,
+                   "parallelism": f"{R} ranks", "receive": "registered (zero copy)",
+                   "l2": "per-rank inputs >= 256 MiB > 126 MB L2, no flush"},
+        "roofline": {"bound": "nvlink_port", "achieved": achieved, "peak": PORT_GBPS, "unit": "GB/s",
+                     "frac": achieved / PORT_GBPS, "traffic": None, "bound_ms": bound_s * 1e3,
+                     "peak_source": "nominal NVLink-5 port, 900 GB/s per direction (north star); "
+                                    "measured peer copy 770 GB/s (B200_PROFILING.md)",
+                     "algorithmic_bytes_per_launch": port_bytes(m, R), "kernel": "nb::exchange_kernel"},
+        "verified": {"mismatched_bytes": mismatches},
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "baselines": {"nccl": nccl},
+    }
+    if mismatches:
+        line["error"] = f"delivery mismatch: {mismatches} bytes"
+    comm.destroy()
+    return line if rank == 0 else None
+
+
+# ------------------------------------------------------------------ reference arm
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    R = 8 if world == 1 else world
+    m = workload_matrix(R, args.per_rank_mib * MiB, args.ratio)
+    v, cores, kind, sample, model = cpu_baseline(R, m, args.cpu_seconds)
+    return {
+        "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sum(m) / (v * 1e9) * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u8", "data": "synthetic: gen_skewed_a2av matrix", "impl": "reference",
+        "config": {"workload": f"skewed all-to-allv, {R} ranks, {args.per_rank_mib} MiB/rank, hotspot ratio "
+                               f"{args.ratio}", "ranks": R, "total_bytes": sum(m)},
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": kind, "sample": sample,
+                         "reference_model_gbps": model},
+        "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="nimble", choices=["nimble", "reference"])
+    ap.add_argument("--per-rank-mib", type=int, default=256)
+    ap.add_argument("--ratio", type=float, default=0.7)
+    ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-baselines", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        line = run_reference(args)
+    elif int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        line = run_multi(args)
+    else:
+        line = run_local(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -142,6 +142,11 @@ nimbleResult_t nimblePlanCreate(nimbleTopology_t topo, int ranks, int ranks_per_
 /* replaces plan_direct_baseline() (planner.hpp:103-104) */
 nimbleResult_t nimblePlanDirect(nimbleTopology_t topo, int ranks, int ranks_per_node,
                                 const uint64_t* matrix, nimblePlan_t* plan);
+/* replaces enumerate_paths() (planner.hpp:86-87): a plan handle holding one
+ * pair (src, dst) with zero demand and no flows, whose candidates are the
+ * enumerated routes (read them with nimblePlanCandidate). */
+nimbleResult_t nimbleEnumeratePaths(nimbleTopology_t topo, int ranks, int ranks_per_node, int src, int dst,
+                                    nimblePlan_t* paths);
 nimbleResult_t nimblePlanDestroy(nimblePlan_t plan);
 nimbleResult_t nimblePlanNumPairs(nimblePlan_t plan, int* npairs);
 nimbleResult_t nimblePlanPair(nimblePlan_t plan, int pair, int* src, int* dst, uint64_t* demand,
@@ -256,6 +261,14 @@ nimbleResult_t nimbleBenchSkewed(nimbleComm_t comm, uint64_t per_rank, double ra
 /* Any R*R matrix (packed layout), e.g. gen_irregular output (collective). */
 nimbleResult_t nimbleBenchMatrix(nimbleComm_t comm, const uint64_t* matrix, int warmup, int iters,
                                  nimbleBenchResult* result);
+
+/* ------------------------------------------------------------- diagnostics */
+
+/* Host-only: join the out-of-band rendezvous of `id` as (rank, nranks), all-
+ * gather `n` bytes per rank into `out` (nranks * n bytes, rank order), leave.
+ * Exercises the bootstrap that nimbleCommInitRank uses, without a GPU. */
+nimbleResult_t nimbleBootstrapAllgather(const nimbleUniqueId* id, int rank, int nranks, const void* in, size_t n,
+                                        void* out);
 
 #ifdef __cplusplus
 }

@@ -74,6 +74,7 @@ SIGNATURES = {
     "nimblePlannerConfigDefault": [P(PlannerConfig)],
     "nimblePlanCreate": [c_void_p, c_int, c_int, P(c_u64), P(PlannerConfig), P(c_void_p)],
     "nimblePlanDirect": [c_void_p, c_int, c_int, P(c_u64), P(c_void_p)],
+    "nimbleEnumeratePaths": [c_void_p, c_int, c_int, c_int, c_int, P(c_void_p)],
     "nimblePlanDestroy": [c_void_p],
     "nimblePlanNumPairs": [c_void_p, P(c_int)],
     "nimblePlanPair": [c_void_p, c_int, P(c_int), P(c_int), P(c_u64), P(c_int), P(c_int)],
@@ -112,6 +113,7 @@ SIGNATURES = {
     "nimbleBenchP2P": [c_void_p, c_u64, c_int, c_int, c_int, c_int, P(BenchResult)],
     "nimbleBenchSkewed": [c_void_p, c_u64, c_double, c_int, c_int, c_int, P(BenchResult)],
     "nimbleBenchMatrix": [c_void_p, P(c_u64), c_int, c_int, P(BenchResult)],
+    "nimbleBootstrapAllgather": [P(UniqueId), c_int, c_int, c_void_p, c_size, c_void_p],
 }
 _RESTYPES = {"nimbleGetErrorString": c_char_p, "nimbleGetLastError": c_char_p}
 

@@ -36,7 +36,7 @@ def _sizes(values):
 def unique_id() -> bytes:
     uid = _lib.UniqueId()
     _lib.call("nimbleGetUniqueId", ctypes.byref(uid))
-    return bytes(uid.internal)
+    return ctypes.string_at(ctypes.addressof(uid), ctypes.sizeof(uid))
 
 
 def comm_config_default() -> _lib.CommConfig:
@@ -59,7 +59,7 @@ class Comm:
     @classmethod
     def init_rank(cls, nranks: int, uid: bytes, rank: int) -> "Comm":
         u = _lib.UniqueId()
-        ctypes.memmove(u.internal, uid, len(uid))
+        ctypes.memmove(ctypes.addressof(u), uid, min(len(uid), ctypes.sizeof(u)))
         h = c_void_p()
         _lib.call("nimbleCommInitRank", ctypes.byref(h), nranks, u, rank)
         return cls(h)

@@ -244,6 +244,24 @@ nimbleResult_t nimblePlanDirect(nimbleTopology_t t, int ranks, int rpn, const ui
     });
 }
 
+nimbleResult_t nimbleEnumeratePaths(nimbleTopology_t t, int ranks, int rpn, int src, int dst, nimblePlan_t* out) {
+    return nb::guarded([&] {
+        if (!t || !out) throw std::invalid_argument("enumerate_paths: null argument");
+        auto* p = new nimblePlan{t->lm, {}};
+        try {
+            nb::PairRoutes pr;
+            pr.src = src;
+            pr.dst = dst;
+            pr.cands = nb::routes_for(t->lm, ranks, rpn, src, dst);
+            p->plan.pairs.push_back(std::move(pr));
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        *out = p;
+    });
+}
+
 nimbleResult_t nimblePlanDestroy(nimblePlan_t p) {
     delete p;
     return nimbleSuccess;

@@ -1075,4 +1075,13 @@ nimbleResult_t nimbleBenchSkewed(nimbleComm_t c, uint64_t per_rank, double ratio
     });
 }
 
+nimbleResult_t nimbleBootstrapAllgather(const nimbleUniqueId* id, int rank, int nranks, const void* in, size_t n,
+                                        void* out) {
+    return guarded([&] {
+        if (!id || (n && (!in || !out))) throw nb::Error(nimbleInvalidArgument, "bootstrap: null argument");
+        auto b = nb::bootstrap_connect(*id, rank, nranks);
+        b->allgather(in, n, out);
+    });
+}
+
 }  // extern "C"

@@ -1,23 +1,37 @@
 // The forwarding engine: one persistent sm_100a kernel per rank per exchange.
 //
-// Every CTA (512 threads) pulls 32-byte work items from the rank's chunk
-// schedule in order (one atomicAdd per item) and moves the item's bytes with
-// 16-byte vector loads/stores, 8 in flight per thread (64 KiB per CTA
-// iteration).  Items are:
+// Each CTA is warp-specialized:
+//   warp 0, lane 0  -- producer: pulls 32-byte work items from the rank's chunk
+//                      schedule in order (one atomicAdd per item), resolves
+//                      where the bytes go (receiver posts, staging slots),
+//                      performs the item's flag waits, and streams the source
+//                      bytes into a ring of shared-memory stages with TMA bulk
+//                      copies (cp.async.bulk global->shared, mbarrier
+//                      complete_tx) -- loads run NS stages ahead with no
+//                      register cost;
+//   warps 1..15     -- consumers: per stage, realign the bytes (source and
+//                      destination may be misaligned relative to each other:
+//                      two 16-byte shared loads + funnel shifts) and store them
+//                      with 16-byte coalesced st.global to the destination --
+//                      local HBM, a peer's registered buffer or a peer's
+//                      staging slot over NVLink; on an item's last stage one
+//                      consumer raises the item's flag (ready / consumed /
+//                      done) after a system-scope fence.
+// Items are:
 //   kLocal   - local copy (self segment, and the 1-GPU emulated exchange);
-//   kPush    - direct push into the receiver's registered buffer over NVLink
-//              (peer stores into IPC-mapped memory), or into the receiver's
-//              self ring when its buffer is not registered;
+//   kPush    - direct push into the receiver's registered buffer over NVLink,
+//              or into the receiver's self ring when its buffer is unregistered;
 //   kStage   - relay hop 1: push into the staging ring hosted on the relay;
-//   kForward - relay hop 2 (or the receiver's own drain of its self ring):
+//   kForward - relay hop 2 (or the receiver's drain of its self ring):
 //              staging slot -> final buffer.
-// Flags follow proj/src/pipeline.cpp:97-106 (see device.cuh).  Waits are
-// polled by one thread per CTA with acquire loads and a global-timer timeout
-// that raises an async error instead of hanging the GPU.
+// Flags follow the reference's bounded-buffer recurrence
+// (proj/src/pipeline.cpp:97-106; device.cuh).  Waits are polled by the
+// producer thread with acquire loads and a global-timer timeout that raises an
+// async error instead of hanging the GPU.
 //
 // Deadlock freedom: the scheduler sorts every rank's items by a global key
 // (chunk progress fraction), every wait targets an item with a strictly
-// smaller key, and CTAs take items in key order -- so the globally smallest
+// smaller key, and items are taken in key order -- so the globally smallest
 // unfinished item always has its dependencies met.
 #include <cuda_runtime.h>
 
@@ -28,6 +42,13 @@
 namespace nb {
 
 namespace {
+
+constexpr int kStageBytes = 32 * 1024;          // bytes of output per stage
+constexpr int kStageVecs = kStageBytes / 16;
+constexpr int kStages = 6;                      // ring depth
+constexpr int kStagePitch = kStageBytes + 128;  // + realignment overhang, 128 B aligned
+constexpr int kConsumerWarps = kThreads / 32 - 1;
+constexpr int kConsumers = kConsumerWarps * 32;
 
 __device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
     uint64_t v;
@@ -45,96 +66,64 @@ __device__ __forceinline__ uint64_t global_ns() {
     return t;
 }
 
-template <bool kStreaming>
-__device__ __forceinline__ uint4 ld16(const uint4* p) {
-    uint4 v;
-    if (kStreaming)  // read-only user buffer: no L1 allocation
-        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                     : "l"(p));
-    else  // staging written by a peer during this kernel: L2 only
-        asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                     : "l"(p));
-    return v;
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ void st16(uint4* p, const uint4& v) {
-    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-                 : "memory");
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
 }
 
-template <bool kStreaming>
-__device__ __forceinline__ uint8_t ld1(const uint8_t* p) {
-    if (kStreaming) return __ldg(p);
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// TMA bulk copy, global -> shared, completion counted on `bar`.
+__device__ __forceinline__ void tma_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(smem)),
+        "l"(gmem), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void st16(void* p, const uint4& v) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+__device__ __forceinline__ uint8_t ld_byte(const uint8_t* p, bool coherent) {
+    if (!coherent) return __ldg(p);
     unsigned short v;
     asm volatile("ld.global.cg.u8 %0, [%1];" : "=h"(v) : "l"(p));
     return static_cast<uint8_t>(v);
 }
 
-constexpr int kUnroll = 8;
+enum AsyncCode : uint32_t {
+    kErrPostTimeout = 1,
+    kErrSlotTimeout = 2,
+    kErrReadyTimeout = 3,
+    kErrDoneTimeout = 4,
+    kErrSizeMismatch = 5,
+    kErrRelayToStaged = 6,
+    kErrFinalTimeout = 7,
+};
 
-// Co-aligned body: src and dst both 16-byte aligned.
-template <bool kStreaming>
-__device__ __forceinline__ void copy_aligned(const uint4* __restrict__ s, uint4* __restrict__ d, uint64_t n16) {
-    uint64_t i = threadIdx.x;
-    for (; i + (kUnroll - 1) * kThreads < n16; i += kUnroll * kThreads) {
-        uint4 v[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) v[u] = ld16<kStreaming>(s + i + u * kThreads);
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) st16(d + i + u * kThreads, v[u]);
-    }
-    for (; i < n16; i += kThreads) st16(d + i, ld16<kStreaming>(s + i));
-}
-
-// dst 16-byte aligned, src off by `sh` (1..15) bytes: two aligned source
-// vectors per output vector, realigned with funnel shifts (q = word shift).
-template <bool kStreaming, int q>
-__device__ __forceinline__ void copy_shifted_q(const uint4* __restrict__ s_al, uint4* __restrict__ d,
-                                               uint64_t n16, uint32_t bits) {
-    for (uint64_t i = threadIdx.x; i < n16; i += kThreads) {
-        const uint4 a = ld16<kStreaming>(s_al + i);
-        const uint4 b = ld16<kStreaming>(s_al + i + 1);
-        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-        uint4 o;
-        o.x = __funnelshift_r(w[q + 0], w[q + 1], bits);
-        o.y = __funnelshift_r(w[q + 1], w[q + 2], bits);
-        o.z = __funnelshift_r(w[q + 2], w[q + 3], bits);
-        o.w = __funnelshift_r(w[q + 3], w[q + 4], bits);
-        st16(d + i, o);
-    }
-}
-
-// CTA-wide copy of n bytes with arbitrary alignment.
-template <bool kStreaming>
-__device__ void cta_copy(const uint8_t* __restrict__ s, uint8_t* __restrict__ d, uint64_t n) {
-    uint64_t head = (16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15;
-    if (head > n) head = n;
-    if (threadIdx.x < head) d[threadIdx.x] = ld1<kStreaming>(s + threadIdx.x);
-    s += head;
-    d += head;
-    n -= head;
-    const uint64_t n16 = n >> 4;
-    const uint32_t sh = reinterpret_cast<uintptr_t>(s) & 15;
-    if (sh == 0) {
-        copy_aligned<kStreaming>(reinterpret_cast<const uint4*>(s), reinterpret_cast<uint4*>(d), n16);
-    } else if (n16) {
-        const uint4* s_al = reinterpret_cast<const uint4*>(s - sh);
-        uint4* dv = reinterpret_cast<uint4*>(d);
-        const uint32_t bits = (sh & 3) * 8;
-        switch (sh >> 2) {
-        case 0: copy_shifted_q<kStreaming, 0>(s_al, dv, n16, bits); break;
-        case 1: copy_shifted_q<kStreaming, 1>(s_al, dv, n16, bits); break;
-        case 2: copy_shifted_q<kStreaming, 2>(s_al, dv, n16, bits); break;
-        default: copy_shifted_q<kStreaming, 3>(s_al, dv, n16, bits); break;
-        }
-    }
-    const uint64_t done = n16 << 4;
-    if (threadIdx.x < n - done) d[done + threadIdx.x] = ld1<kStreaming>(s + done + threadIdx.x);
-}
-
-// Single-thread wait until *p >= tag; false (and an async error) on timeout
+// Producer-thread wait until *p >= tag; false (and an async error) on timeout
 // or when another wait already failed.
 __device__ bool wait_ge(const uint64_t* p, uint64_t tag, const CommDevice* c, uint32_t code) {
     if (ld_acquire(p) >= tag) return true;
@@ -156,26 +145,42 @@ __device__ bool wait_ge(const uint64_t* p, uint64_t tag, const CommDevice* c, ui
 
 __device__ __forceinline__ uint64_t tag_of(uint64_t epoch, uint32_t k) { return (epoch << 32) | (k + 1ull); }
 
-enum AsyncCode : uint32_t {
-    kErrPostTimeout = 1,
-    kErrSlotTimeout = 2,
-    kErrReadyTimeout = 3,
-    kErrDoneTimeout = 4,
-    kErrSizeMismatch = 5,
-    kErrRelayToStaged = 6,
-    kErrFinalTimeout = 7,
+enum StageFlags : uint32_t {
+    kTerminate = 1,
+    kItemEnd = 2,      // last stage of an item: head/tail bytes + end actions
+    kCoherentSrc = 4,  // source written by a peer during this launch (staging)
+};
+
+enum EndAction : uint32_t {
+    kActRelease1 = 1,  // st.release(flag1, tag1)
+    kActRelease2 = 2,  // st.release(flag2, tag2)
+    kActCount = 4,     // count a write into receiver count_d; publish done on the last
+};
+
+struct StageDesc {
+    uint64_t dst;    // 16-byte aligned destination of the stage's first vector
+    uint32_t nvec;   // 16-byte output vectors in the stage
+    uint32_t shift;  // source misalignment (0..15) of the body
+    uint32_t flags;
+    uint32_t action;
+    uint64_t head_src, head_dst, tail_src, tail_dst;
+    uint32_t head_n, tail_n;
+    uint64_t* flag1;
+    uint64_t tag1;
+    uint64_t* flag2;
+    uint64_t tag2;
+    uint32_t count_d, count_target;
 };
 
 struct SharedState {
-    uint64_t seg_base[kMaxRanks * kMaxRanks];  // (receiver, sender) -> resolved segment base, 0 = unresolved
-    uint32_t seg_mode[kMaxRanks * kMaxRanks];
-    Item item;
-    uint64_t src, dst;
-    uint32_t index;
-    uint32_t ok;
+    uint64_t full[kStages];
+    uint64_t empty[kStages];
+    StageDesc desc[kStages];
+    uint64_t seg_base[kMaxRanks * kMaxRanks];  // (receiver, sender) -> resolved segment base
+    uint32_t seg_mode[kMaxRanks * kMaxRanks];  // 0 = unresolved
 };
 
-// Resolve receiver d's post for sender s (thread 0 only).
+// Resolve receiver d's post for sender s (producer thread).
 __device__ bool resolve(SharedState& sh, const LaunchArgs& a, int d, int s) {
     const int key = d * kMaxRanks + s;
     if (sh.seg_mode[key]) return true;
@@ -203,34 +208,235 @@ __device__ __forceinline__ uint8_t* ring_slot(const LaunchArgs& a, int host, int
     return a.comm->staging[host] + (ring * a.slots + seq % a.slots) * a.pipe_chunk;
 }
 
-// After a CTA finished an item that wrote into receiver d's memory: count it
-// and, on the receiver's last item from this rank, publish done[me] = epoch.
-__device__ void count_write(SharedState& sh, const LaunchArgs& a, int d, uint32_t* counters) {
-    const int me = a.comm->rank;
+__device__ __forceinline__ uint64_t* ctrl_flag(const LaunchArgs& a, int rank, uint64_t off) {
+    return reinterpret_cast<uint64_t*>(a.comm->ctrl[rank] + off);
+}
+
+// Producer: the item's source, destination and end-of-item actions.  False
+// when the item must be skipped (a wait failed; the error is latched).
+__device__ bool prepare(SharedState& sh, const LaunchArgs& a, const Item& it, uint64_t& src, uint64_t& dst,
+                        StageDesc& end, bool& coherent) {
+    const CommDevice* c = a.comm;
+    const int me = c->rank, R = c->nranks;
+    src = it.src;
+    dst = it.dst;
+    coherent = false;
+    end.action = 0;
+    if (it.kind == kLocal) return true;
+    if (it.kind == kPush || it.kind == kStage) {
+        const int host = it.peer;  // receiver (push) or relay (stage)
+        const int d = it.kind == kPush ? it.peer : it.aux;
+        if (it.kind == kPush) {
+            if (!resolve(sh, a, d, me)) return false;
+            if (sh.seg_mode[d * kMaxRanks + me] == kPostZeroCopy) {
+                dst = sh.seg_base[d * kMaxRanks + me] + it.dst;
+                end.action = kActCount;
+                end.count_d = d;
+                end.count_target = a.fwd_items[d] + a.push_items[d];
+                return true;
+            }
+        }
+        const uint32_t slot = it.seq % a.slots;
+        if (it.seq >= a.slots &&
+            !wait_ge(ctrl_flag(a, me, FlagLayout::consumed_off(R, d, host, slot)), tag_of(a.epoch, it.seq - a.slots), c,
+                     kErrSlotTimeout))
+            return false;
+        dst = reinterpret_cast<uint64_t>(ring_slot(a, host, me, d, it.seq));
+        end.action = kActRelease1;  // chunk landed in the slot: raise its ready flag
+        end.flag1 = ctrl_flag(a, host, FlagLayout::ready_off(R, me, d, slot));
+        end.tag1 = tag_of(a.epoch, it.seq);
+        return true;
+    }
+    // kForward: ring (s, d) hosted here -> receiver d
+    const int s = it.aux, d = it.peer;
+    const uint32_t slot = it.seq % a.slots;
+    if (!wait_ge(ctrl_flag(a, me, FlagLayout::ready_off(R, s, d, slot)), tag_of(a.epoch, it.seq), c, kErrReadyTimeout))
+        return false;
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // peer-written slot, read by TMA
+    coherent = true;
+    src = reinterpret_cast<uint64_t>(ring_slot(a, me, s, d, it.seq));
+    end.action = kActRelease2;  // the slot is drained: hand it back to the stager
+    end.flag2 = ctrl_flag(a, s, FlagLayout::consumed_off(R, d, me, slot));
+    end.tag2 = tag_of(a.epoch, it.seq);
+    if (d == me) {
+        dst = a.posts[s].off + it.dst;  // staged self receive: absolute local address
+        return true;
+    }
+    if (!resolve(sh, a, d, s)) return false;
+    if (sh.seg_mode[d * kMaxRanks + s] != kPostZeroCopy) {
+        atomicCAS(c->status, 0u, static_cast<uint32_t>(kErrRelayToStaged));
+        return false;
+    }
+    dst = sh.seg_base[d * kMaxRanks + s] + it.dst;
     uint32_t target = a.fwd_items[d];
-    if (a.push_items[d]) {  // my pushes count only if d takes them in place
-        if (!resolve(sh, a, d, me)) return;
+    if (a.push_items[d]) {  // my own pushes to d count only if d takes them in place
+        if (!resolve(sh, a, d, me)) return false;
         if (sh.seg_mode[d * kMaxRanks + me] == kPostZeroCopy) target += a.push_items[d];
     }
-    __threadfence_system();
-    const uint32_t prev = atomicAdd(&counters[d], 1u);
-    if (prev + 1 == target) {
-        CtrlHeader* h = reinterpret_cast<CtrlHeader*>(a.comm->ctrl[d]);
-        st_release(&h->done[me], a.epoch);
+    end.action |= kActCount;
+    end.count_d = d;
+    end.count_target = target;
+    return true;
+}
+
+__device__ void produce(SharedState& sh, uint8_t* stages, const LaunchArgs& a) {
+    uint32_t* scratch = a.comm->scratch;
+    uint32_t cnt = 0;
+    auto next_slot = [&](uint32_t& slot) {
+        slot = cnt % kStages;
+        if (cnt >= kStages) mbar_wait(&sh.empty[slot], ((cnt / kStages) - 1) & 1);
+    };
+    for (;;) {
+        const uint32_t index = atomicAdd(&scratch[0], 1u);
+        if (index >= a.nitems) break;
+        const Item it = a.items[index];
+        uint64_t src, dst;
+        StageDesc end{};
+        bool coherent = false;
+        if (!prepare(sh, a, it, src, dst, end, coherent)) continue;
+        // head: bytes until the destination is 16-byte aligned
+        uint64_t n = it.bytes;
+        uint32_t head = static_cast<uint32_t>((16 - (dst & 15)) & 15);
+        if (head > n) head = static_cast<uint32_t>(n);
+        const uint64_t bsrc = src + head, bdst = dst + head;
+        n -= head;
+        const uint64_t n16 = n >> 4;
+        const uint32_t tail = static_cast<uint32_t>(n & 15);
+        const uint32_t shift = static_cast<uint32_t>(bsrc & 15);
+        const uint64_t src_al = bsrc - shift;
+        const uint64_t src_al_end = (bsrc + (n16 << 4) + 15) & ~15ull;
+        const uint64_t nstages = n16 ? (n16 + kStageVecs - 1) / kStageVecs : 1;
+        for (uint64_t k = 0; k < nstages; ++k) {
+            uint32_t slot;
+            next_slot(slot);
+            StageDesc& ds = sh.desc[slot];
+            const uint64_t v0 = k * kStageVecs;
+            const uint32_t nvec = static_cast<uint32_t>(n16 > v0 ? (n16 - v0 < kStageVecs ? n16 - v0 : kStageVecs) : 0);
+            ds.dst = bdst + (v0 << 4);
+            ds.nvec = nvec;
+            ds.shift = shift;
+            ds.flags = coherent ? kCoherentSrc : 0;
+            if (k + 1 == nstages) {
+                ds.flags |= kItemEnd;
+                ds.action = end.action;
+                ds.head_src = src;
+                ds.head_dst = dst;
+                ds.head_n = head;
+                ds.tail_src = bsrc + (n16 << 4);
+                ds.tail_dst = bdst + (n16 << 4);
+                ds.tail_n = tail;
+                ds.flag1 = end.flag1;
+                ds.tag1 = end.tag1;
+                ds.flag2 = end.flag2;
+                ds.tag2 = end.tag2;
+                ds.count_d = end.count_d;
+                ds.count_target = end.count_target;
+            }
+            uint32_t bytes = 0;
+            if (nvec) {
+                const uint64_t from = src_al + (v0 << 4);
+                const uint64_t want = (static_cast<uint64_t>(nvec) << 4) + (shift ? 16 : 0);
+                bytes = static_cast<uint32_t>(src_al_end - from < want ? src_al_end - from : want);
+            }
+            if (bytes) {
+                mbar_arrive_tx(&sh.full[slot], bytes);
+                tma_load(stages + slot * kStagePitch, reinterpret_cast<const void*>(src_al + (v0 << 4)), bytes,
+                         &sh.full[slot]);
+            } else {
+                mbar_arrive(&sh.full[slot]);
+            }
+            ++cnt;
+        }
+    }
+    uint32_t slot;
+    next_slot(slot);
+    sh.desc[slot].flags = kTerminate;
+    mbar_arrive(&sh.full[slot]);
+}
+
+template <int q>
+__device__ __forceinline__ void realign_store(const uint4* buf, uint8_t* out, uint32_t nvec, uint32_t bits, int ct) {
+    for (uint32_t j = ct; j < nvec; j += kConsumers) {
+        const uint4 x = buf[j], y = buf[j + 1];
+        const uint32_t w[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+        uint4 o;
+        o.x = __funnelshift_r(w[q + 0], w[q + 1], bits);
+        o.y = __funnelshift_r(w[q + 1], w[q + 2], bits);
+        o.z = __funnelshift_r(w[q + 2], w[q + 3], bits);
+        o.w = __funnelshift_r(w[q + 3], w[q + 4], bits);
+        st16(out + 16ull * j, o);
     }
 }
+
+__device__ void consume(SharedState& sh, const uint8_t* stages, const LaunchArgs& a) {
+    const int ct = threadIdx.x - 32;  // consumer thread index
+    const int lane = threadIdx.x & 31;
+    uint32_t* counters = a.comm->scratch + 2;
+    for (uint32_t cnt = 0;; ++cnt) {
+        const uint32_t slot = cnt % kStages;
+        mbar_wait(&sh.full[slot], (cnt / kStages) & 1);
+        const StageDesc ds = sh.desc[slot];
+        if (ds.flags & kTerminate) break;
+        const uint4* buf = reinterpret_cast<const uint4*>(stages + slot * kStagePitch);
+        uint8_t* out = reinterpret_cast<uint8_t*>(ds.dst);
+        const uint32_t bits = (ds.shift & 3) * 8;
+        switch (ds.shift ? 1 + (ds.shift >> 2) : 0) {  // uniform across the CTA
+        case 0:
+            for (uint32_t j = ct; j < ds.nvec; j += kConsumers) st16(out + 16ull * j, buf[j]);
+            break;
+        case 1: realign_store<0>(buf, out, ds.nvec, bits, ct); break;
+        case 2: realign_store<1>(buf, out, ds.nvec, bits, ct); break;
+        case 3: realign_store<2>(buf, out, ds.nvec, bits, ct); break;
+        default: realign_store<3>(buf, out, ds.nvec, bits, ct); break;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sh.empty[slot]);
+        if (ds.flags & kItemEnd) {
+            const bool coh = ds.flags & kCoherentSrc;
+            if (ct < static_cast<int>(ds.head_n))
+                reinterpret_cast<uint8_t*>(ds.head_dst)[ct] = ld_byte(reinterpret_cast<const uint8_t*>(ds.head_src) + ct, coh);
+            if (ct >= 32 && ct < 32 + static_cast<int>(ds.tail_n))
+                reinterpret_cast<uint8_t*>(ds.tail_dst)[ct - 32] =
+                    ld_byte(reinterpret_cast<const uint8_t*>(ds.tail_src) + (ct - 32), coh);
+            asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+            if (ct == 0 && ds.action) {
+                __threadfence_system();
+                if (ds.action & kActRelease1) st_release(ds.flag1, ds.tag1);
+                if (ds.action & kActRelease2) st_release(ds.flag2, ds.tag2);
+                if (ds.action & kActCount) {
+                    const uint32_t prev = atomicAdd(&counters[ds.count_d], 1u);
+                    if (prev + 1 == ds.count_target) {
+                        CtrlHeader* h = reinterpret_cast<CtrlHeader*>(a.comm->ctrl[ds.count_d]);
+                        st_release(&h->done[a.comm->rank], a.epoch);
+                    }
+                }
+            }
+        }
+    }
+}
+
+constexpr size_t kEngineSmem = sizeof(SharedState) + 128 + static_cast<size_t>(kStages) * kStagePitch;
 
 }  // namespace
 
 __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_constant__ LaunchArgs a) {
-    __shared__ SharedState sh;
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    SharedState& sh = *reinterpret_cast<SharedState*>(smem_raw);
+    uint8_t* stages = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw + sizeof(SharedState)) + 127) & ~static_cast<uintptr_t>(127));
     const CommDevice* c = a.comm;
     const int tid = threadIdx.x;
     uint32_t* scratch = c->scratch;
-    uint32_t* counters = scratch + 2;
     const int me = c->rank, R = c->nranks;
 
     for (int i = tid; i < kMaxRanks * kMaxRanks; i += kThreads) sh.seg_mode[i] = 0;
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&sh.full[s], 1);
+            mbar_init(&sh.empty[s], kConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     // Prologue: publish where each sender's segment lands in my buffer.
     if (!a.local_only && blockIdx.x == 0 && tid < R) {
         const Post p = a.posts[tid];
@@ -240,90 +446,19 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
             mine->mode = p.mode;
             mine->off = p.off;
             mine->bytes = p.bytes;
-            st_release(&mine->tag, p.tag);
+            st_release(&mine->tag, a.epoch);
         }
     }
     __syncthreads();
 
-    for (;;) {
-        if (tid == 0) {
-            sh.index = atomicAdd(&scratch[0], 1u);
-            sh.ok = 1;
-            if (sh.index < a.nitems) {
-                const Item it = a.items[sh.index];
-                sh.item = it;
-                uint64_t src = it.src, dst = it.dst;
-                if (it.kind == kPush || it.kind == kStage) {
-                    const int host = it.peer;  // receiver (push) or relay (stage)
-                    const int d = it.kind == kPush ? it.peer : it.aux;
-                    bool staged = it.kind == kStage;
-                    if (it.kind == kPush) {
-                        sh.ok = resolve(sh, a, d, me);
-                        staged = sh.ok && sh.seg_mode[d * kMaxRanks + me] == kPostStaged;
-                        if (sh.ok && !staged) dst = sh.seg_base[d * kMaxRanks + me] + it.dst;
-                    }
-                    if (sh.ok && staged) {
-                        if (it.seq >= a.slots) {
-                            const uint64_t* f = reinterpret_cast<const uint64_t*>(
-                                c->ctrl[me] + FlagLayout::consumed_off(R, d, host, it.seq % a.slots));
-                            sh.ok = wait_ge(f, tag_of(a.epoch, it.seq - a.slots), c, kErrSlotTimeout);
-                        }
-                        dst = reinterpret_cast<uint64_t>(ring_slot(a, host, me, d, it.seq));
-                    }
-                } else if (it.kind == kForward) {
-                    const int s = it.aux, d = it.peer;
-                    const uint64_t* f =
-                        reinterpret_cast<const uint64_t*>(c->ctrl[me] + FlagLayout::ready_off(R, s, d, it.seq % a.slots));
-                    sh.ok = wait_ge(f, tag_of(a.epoch, it.seq), c, kErrReadyTimeout);
-                    src = reinterpret_cast<uint64_t>(ring_slot(a, me, s, d, it.seq));
-                    if (d == me) {
-                        dst = a.posts[s].off + it.dst;  // staged self receive: absolute local address
-                    } else if (sh.ok) {
-                        sh.ok = resolve(sh, a, d, s);
-                        if (sh.ok && sh.seg_mode[d * kMaxRanks + s] != kPostZeroCopy) {
-                            atomicCAS(c->status, 0u, static_cast<uint32_t>(kErrRelayToStaged));
-                            sh.ok = 0;
-                        }
-                        if (sh.ok) dst = sh.seg_base[d * kMaxRanks + s] + it.dst;
-                    }
-                }
-                sh.src = src;
-                sh.dst = dst;
-            }
-        }
-        __syncthreads();
-        if (sh.index >= a.nitems) break;
-        const Item it = sh.item;
-        if (sh.ok) {
-            if (it.kind == kForward)
-                cta_copy<false>(reinterpret_cast<const uint8_t*>(sh.src), reinterpret_cast<uint8_t*>(sh.dst), it.bytes);
-            else
-                cta_copy<true>(reinterpret_cast<const uint8_t*>(sh.src), reinterpret_cast<uint8_t*>(sh.dst), it.bytes);
-        }
-        __syncthreads();
-        if (tid == 0 && sh.ok) {
-            if (it.kind == kPush || it.kind == kStage) {
-                const int d = it.kind == kPush ? it.peer : it.aux;
-                const bool staged = it.kind == kStage || sh.seg_mode[d * kMaxRanks + me] == kPostStaged;
-                if (staged) {  // chunk landed in the ring slot: raise its ready flag
-                    __threadfence_system();
-                    uint64_t* f = reinterpret_cast<uint64_t*>(c->ctrl[it.peer] +
-                                                              FlagLayout::ready_off(R, me, d, it.seq % a.slots));
-                    st_release(f, tag_of(a.epoch, it.seq));
-                } else {
-                    count_write(sh, a, d, counters);
-                }
-            } else if (it.kind == kForward) {
-                const int s = it.aux, d = it.peer;
-                // the slot's bytes are all read (stores issued): hand it back to the stager
-                uint64_t* f = reinterpret_cast<uint64_t*>(c->ctrl[s] + FlagLayout::consumed_off(R, d, me, it.seq % a.slots));
-                if (d != me) count_write(sh, a, d, counters);
-                st_release(f, tag_of(a.epoch, it.seq));
-            }
-        }
+    if (tid < 32) {
+        if (tid == 0) produce(sh, stages, a);
+    } else {
+        consume(sh, stages, a);
     }
+    __syncthreads();
 
-    // Epilogue: the last CTA out waits for (a) my staged chunks to be drained
+    // Epilogue: the last CTA out waits for (a) my relayed chunks to be drained
     // from their rings, (b) every writer into my buffer to report done; then
     // resets the per-launch scratch for the next stream-ordered launch.
     if (tid == 0) {
@@ -332,11 +467,13 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
         if (arrived + 1 == gridDim.x) {
             if (!a.local_only) {
                 for (uint32_t i = 0; i < a.nfinal; ++i)
-                    wait_ge(reinterpret_cast<const uint64_t*>(c->ctrl[me] + a.final_waits[2 * i]), tag_of(a.epoch, static_cast<uint32_t>(a.final_waits[2 * i + 1])), c, kErrFinalTimeout);
+                    wait_ge(reinterpret_cast<const uint64_t*>(c->ctrl[me] + a.final_waits[2 * i]),
+                            tag_of(a.epoch, static_cast<uint32_t>(a.final_waits[2 * i + 1])), c, kErrFinalTimeout);
                 const CtrlHeader* h = reinterpret_cast<const CtrlHeader*>(c->ctrl[me]);
                 for (int w = 0; w < R; ++w)
                     if ((a.expect_done >> w) & 1) wait_ge(&h->done[w], a.epoch, c, kErrDoneTimeout);
             }
+            uint32_t* counters = scratch + 2;
             for (int d = 0; d < R; ++d) counters[d] = 0;
             scratch[0] = 0;
             __threadfence();
@@ -396,7 +533,16 @@ __global__ void check_kernel(const uint8_t* buf, uint64_t first, uint64_t n, uin
 // ---- host-side launchers (called from the comm runtime) ----
 
 cudaError_t launch_exchange(const LaunchArgs& args, int ctas, cudaStream_t stream) {
-    exchange_kernel<<<ctas, kThreads, 0, stream>>>(args);
+    static thread_local int configured_device = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured_device != dev) {  // opt in to > 48 KB of dynamic shared memory (per device)
+        cudaError_t e = cudaFuncSetAttribute(exchange_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(kEngineSmem));
+        if (e != cudaSuccess) return e;
+        configured_device = dev;
+    }
+    exchange_kernel<<<ctas, kThreads, kEngineSmem, stream>>>(args);
     return cudaGetLastError();
 }
 

@@ -279,15 +279,13 @@ def plan_direct_baseline(topo: Topology, ranks, ranks_per_node, matrix) -> Plan:
 
 
 def enumerate_paths(topo: Topology, ranks, ranks_per_node, src, dst):
-    """enumerate_paths() -- planner.hpp:86-87 (through a one-pair direct plan)."""
-    m = [0] * (ranks * ranks)
-    if not (0 <= src < ranks and 0 <= dst < ranks) or src == dst:
-        m2 = [0] * (ranks * ranks)
-        if 0 <= src < ranks and 0 <= dst < ranks:
-            m2[src * ranks + dst] = 1  # nonzero diagonal -> error from the library
-        return plan_direct_baseline(topo, ranks, ranks_per_node, m2).pairs[0].candidates
-    m[src * ranks + dst] = 1
-    return plan_direct_baseline(topo, ranks, ranks_per_node, m).pairs[0].candidates
+    """enumerate_paths() -- planner.hpp:86-87."""
+    h = c_void_p()
+    _lib.call("nimbleEnumeratePaths", topo.handle, ranks, ranks_per_node, src, dst, ctypes.byref(h))
+    try:
+        return _read_plan(h, topo.link_count()).pairs[0].candidates
+    finally:
+        _lib.lib().nimblePlanDestroy(h)
 
 
 def plan_link_loads(p: Plan):
