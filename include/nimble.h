@@ -183,7 +183,10 @@ typedef struct {
     uint64_t p2p_buffer;          /* staging bytes per ring, 10 MiB (pipeline.hpp:18)   */
     int channels_per_peer;        /* rings per relayed flow, 1 (pipeline.hpp:23)        */
     int ctas;                     /* forwarding-engine CTAs per launch, 0 = auto        */
-    uint64_t direct_chunk;        /* work-item size for direct pushes, 0 = auto         */
+    uint64_t direct_chunk;        /* work-item size for local copies, 0 = auto          */
+    int pull;                     /* receiver-driven pulls: 0 = auto (a rank whose ingress
+                                     exceeds its egress pulls from registered senders),
+                                     1 = never, 2 = always when the sender is registered */
 } nimbleCommConfig;
 
 nimbleResult_t nimbleCommConfigDefault(nimbleCommConfig* cfg);

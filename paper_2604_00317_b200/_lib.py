@@ -38,7 +38,7 @@ class PlanStats(ctypes.Structure):  # nimblePlanStats
 class CommConfig(ctypes.Structure):  # nimbleCommConfig
     _fields_ = [("fabric", c_int), ("gpus_per_node", c_int), ("nvlink_bytes_per_s", c_double),
                 ("planner", PlannerConfig), ("pipe_chunk", c_u64), ("p2p_buffer", c_u64),
-                ("channels_per_peer", c_int), ("ctas", c_int), ("direct_chunk", c_u64)]
+                ("channels_per_peer", c_int), ("ctas", c_int), ("direct_chunk", c_u64), ("pull", c_int)]
 
 
 class UniqueId(ctypes.Structure):  # nimbleUniqueId

@@ -168,6 +168,7 @@ struct CachedSchedule {
     Schedule sc;
     DevBuf<Item> items;
     DevBuf<Post> posts;
+    DevBuf<Post> send_posts;
     DevBuf<uint64_t> finals;
 };
 
@@ -285,6 +286,7 @@ void default_config(nimbleCommConfig* cfg, int nranks) {
     cfg->channels_per_peer = 1;
     cfg->ctas = 0;
     cfg->direct_chunk = 0;
+    cfg->pull = 0;
 }
 
 // Allocate ctrl + staging, exchange handles / pointers, map peers.
@@ -329,8 +331,8 @@ void setup_common(nimbleComm* c) {
     CUDA_TRY(cudaMalloc(&c->d_view, sizeof(CommDevice)));
     CUDA_TRY(cudaMalloc(&c->d_win_table, sizeof(uint64_t) * kMaxWindows * kMaxRanks));
     CUDA_TRY(cudaMemset(c->d_win_table, 0, sizeof(uint64_t) * kMaxWindows * kMaxRanks));
-    CUDA_TRY(cudaMalloc(&c->d_scratch, sizeof(uint32_t) * (2 + kMaxRanks)));
-    CUDA_TRY(cudaMemset(c->d_scratch, 0, sizeof(uint32_t) * (2 + kMaxRanks)));
+    CUDA_TRY(cudaMalloc(&c->d_scratch, sizeof(uint32_t) * (2 + 2 * kMaxRanks)));
+    CUDA_TRY(cudaMemset(c->d_scratch, 0, sizeof(uint32_t) * (2 + 2 * kMaxRanks)));
     CUDA_TRY(cudaHostAlloc(&c->h_status, 64, cudaHostAllocMapped | cudaHostAllocPortable));
     std::memset(c->h_status, 0, 64);
     CUDA_TRY(cudaHostGetDevicePointer(&c->d_status, c->h_status, 0));
@@ -438,9 +440,38 @@ Exchange make_exchange(nimbleComm* c, const std::vector<PendingOp*>& ops) {
     return ex;
 }
 
+// Registered window holding [ptr, ptr + n), or -1.
+int window_of(const nimbleComm* c, uint64_t ptr, uint64_t n) {
+    for (size_t w = 0; w < c->windows.size(); ++w) {
+        const Window& win = c->windows[w];
+        if (win.live && ptr >= win.base && ptr + n <= win.base + win.size) return static_cast<int>(w);
+    }
+    return -1;
+}
+
 // Where each incoming segment lands: a registered window (zero copy) or the
-// self ring (staged).
+// self ring (staged); where each outgoing segment lives (registered windows
+// can be pulled by their receiver); whether this rank asks to pull.
 void fill_posts(nimbleComm* c, RankBuffers& rb) {
+    uint64_t ingress = 0, egress = 0;
+    for (int p = 0; p < rb.R; ++p)
+        if (p != rb.me) ingress += rb.recv_bytes[p], egress += rb.send_bytes[p];
+    rb.pull = c->cfg.pull == 2 || (c->cfg.pull == 0 && ingress > egress);
+    rb.send_post.assign(static_cast<size_t>(rb.R), Post{});
+    for (int d = 0; d < rb.R; ++d) {
+        if (d == rb.me || rb.send_bytes[d] == 0) continue;
+        Post p{};
+        p.tag = 1;
+        p.bytes = rb.send_bytes[d];
+        p.mode = kSendPlain;
+        const int w = window_of(c, rb.send_ptr[d], rb.send_bytes[d]);
+        if (w >= 0) {
+            p.mode = kSendRegistered;
+            p.win = static_cast<uint32_t>(w);
+            p.off = rb.send_ptr[d] - c->windows[static_cast<size_t>(w)].base;
+        }
+        rb.send_post[static_cast<size_t>(d)] = p;
+    }
     rb.recv_post.assign(static_cast<size_t>(rb.R), Post{});
     for (int s = 0; s < rb.R; ++s) {
         if (s == rb.me || rb.recv_bytes[s] == 0) continue;
@@ -449,15 +480,13 @@ void fill_posts(nimbleComm* c, RankBuffers& rb) {
         p.bytes = rb.recv_bytes[s];
         p.mode = kPostStaged;
         p.off = rb.recv_ptr[s];
-        for (size_t w = 0; w < c->windows.size(); ++w) {
-            const Window& win = c->windows[w];
-            if (win.live && rb.recv_ptr[s] >= win.base && rb.recv_ptr[s] + rb.recv_bytes[s] <= win.base + win.size) {
-                p.mode = kPostZeroCopy;
-                p.win = static_cast<uint32_t>(w);
-                p.off = rb.recv_ptr[s] - win.base;
-                break;
-            }
+        const int w = window_of(c, rb.recv_ptr[s], rb.recv_bytes[s]);
+        if (w >= 0) {
+            p.mode = kPostZeroCopy;
+            p.win = static_cast<uint32_t>(w);
+            p.off = rb.recv_ptr[s] - c->windows[static_cast<size_t>(w)].base;
         }
+        if (rb.pull) p.mode |= kPostPullRequest;
         rb.recv_post[static_cast<size_t>(s)] = p;
     }
 }
@@ -473,6 +502,8 @@ CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& 
         key.push_back(rb.recv_bytes[r]);
         key.push_back(rb.recv_post[r].mode);
         key.push_back(rb.recv_post[r].win);
+        key.push_back(rb.send_post[r].mode);
+        key.push_back(rb.send_post[r].win);
     }
     for (auto it = c->schedules.begin(); it != c->schedules.end(); ++it)
         if (it->key == key) {
@@ -488,11 +519,13 @@ CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& 
         CachedSchedule& old = c->schedules.back();
         cs.items = std::move(old.items);
         cs.posts = std::move(old.posts);
+        cs.send_posts = std::move(old.send_posts);
         cs.finals = std::move(old.finals);
         c->schedules.pop_back();
     }
     cs.items.assign(cs.sc.items, st);
     cs.posts.assign(cs.sc.posts, st);
+    cs.send_posts.assign(cs.sc.send_posts, st);
     cs.finals.assign(cs.sc.final_waits, st);
     c->schedules.push_front(std::move(cs));
     return c->schedules.front();
@@ -507,12 +540,18 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     a.epoch = ++c->epoch;
     a.comm = c->d_view;
     a.posts = cs.posts.p;
+    a.send_posts = cs.send_posts.p;
     for (int r = 0; r < c->nranks; ++r) {
         a.push_items[r] = cs.sc.push_items[r];
         a.fwd_items[r] = cs.sc.fwd_items[r];
+        a.pull_items[r] = cs.sc.pull_items[r];
         a.send_bytes[r] = rb.send_bytes[r];
     }
-    a.expect_done = cs.sc.expect_done;
+    a.recv_direct = cs.sc.recv_direct;
+    a.recv_zc = cs.sc.recv_zc;
+    a.pull_req = cs.sc.pull_req;
+    a.relay_writers = cs.sc.relay_writers;
+    a.push_targets = cs.sc.push_targets;
     a.final_waits = cs.finals.p;
     a.nfinal = static_cast<uint32_t>(cs.sc.final_waits.size() / 2);
     a.local_only = 0;
@@ -691,8 +730,8 @@ void bench_matrix(nimbleComm* c, const std::vector<uint64_t>& m, int warmup, int
     const uint64_t seed = 1;
     cudaStream_t st = c->bench_stream;
     for (int p = 0; p < R; ++p) CUDA_TRY(launch_fill(sbuf + sd[p], 0, sc[p], seed, me, p, st));
-    void* handle = register_window(c, rbuf, std::max<size_t>(rtot, 16));
-    (void)handle;
+    register_window(c, rbuf, std::max<size_t>(rtot, 16));
+    register_window(c, sbuf, std::max<size_t>(stot, 16));  // ingress-heavy receivers may pull
     auto once = [&] {
         nimbleResult_t r = nimbleAlltoAllv(sbuf, sc.data(), sd.data(), rbuf, rc.data(), rd.data(), nimbleUint8, c, st);
         if (r != nimbleSuccess) throw Error(r, g_last_error);
@@ -761,9 +800,11 @@ void bench_matrix(nimbleComm* c, const std::vector<uint64_t>& m, int warmup, int
             for (const Flow& f : p.flows) out->relay_flows += p.cands[static_cast<size_t>(f.cand)].via >= 0;
     }
     c->boot->barrier();
-    c->windows.back().live = false;
-    for (void* p : c->windows.back().opened) ipc_cache().release(p);
-    c->windows.back().opened.clear();
+    for (size_t k = c->windows.size() - 2; k < c->windows.size(); ++k) {
+        c->windows[k].live = false;
+        for (void* p : c->windows[k].opened) ipc_cache().release(p);
+        c->windows[k].opened.clear();
+    }
     c->schedules.clear();
     cudaFree(sbuf);
     cudaFree(rbuf);

@@ -33,24 +33,34 @@ enum ItemKind : uint8_t {
     kPush = 1,     // my send range -> receiver `peer` (zero copy, or its self ring when staged)
     kStage = 2,    // my send range -> ring (me, aux) hosted on relay `peer`
     kForward = 3,  // ring (aux, peer) hosted here -> receiver `peer` (or my own buffer)
+    kPull = 4,     // sender `peer`'s registered send range -> my buffer (receiver-driven)
 };
 
 // One unit of the chunk schedule, 32 bytes.
 struct Item {
-    uint64_t src;    // kLocal/kPush/kStage: absolute local source address
-    uint64_t dst;    // kLocal: absolute; kPush/kForward: byte offset inside the pair segment
+    uint64_t src;    // kLocal/kPush/kStage: absolute local source address; kPull: offset in the segment
+    uint64_t dst;    // kLocal/kPull: absolute; kPush/kForward: byte offset inside the pair segment
     uint32_t bytes;  // <= pipe_chunk for ring traffic
     uint8_t kind;
-    uint8_t peer;    // kLocal: unused; kPush: receiver; kStage: relay; kForward: final receiver
+    uint8_t peer;    // kLocal: unused; kPush: receiver; kStage: relay; kForward: final receiver; kPull: sender
     uint16_t aux;    // kStage: final receiver; kForward: original sender
     uint32_t seq;    // chunk index in the ring / flow
     uint32_t pad;
 };
 static_assert(sizeof(Item) == 32, "Item layout");
 
-enum PostMode : uint32_t { kPostZeroCopy = 1, kPostStaged = 2 };
+// Receive posts: where a sender's segment lands (+ a pull request bit).
+// Send posts: where my outgoing segment lives, if it is registered.
+enum PostMode : uint32_t {
+    kPostZeroCopy = 1,
+    kPostStaged = 2,
+    kPostPullRequest = 0x10,  // receiver asks the sender to let it pull
+    kSendRegistered = 1,      // send post: segment readable by the receiver (window win, offset off)
+    kSendPlain = 2,           // send post: not registered, the sender pushes
+};
 
-// Receiver d publishes, for each sender s, where s's segment lands.
+// Receiver d publishes, for each sender s, where s's segment lands; sender s
+// publishes, for each receiver d, where its outgoing segment lives.
 struct Post {
     uint64_t tag;    // epoch of the call this post belongs to
     uint32_t win;    // registered window id (zero copy)
@@ -63,6 +73,8 @@ static_assert(sizeof(Post) == 32, "Post layout");
 struct CtrlHeader {
     Post post[kMaxRanks];       // written by me (the receiver), read by writers
     uint64_t done[kMaxRanks];   // done[w] = epoch: writer w finished writing into me
+    Post send_post[kMaxRanks];  // written by me (the sender), read by pulling receivers
+    uint64_t pulled[kMaxRanks]; // pulled[d] = epoch: receiver d finished pulling from me
 };
 
 // Geometry of the flag arrays that follow the header inside ctrl.
@@ -89,7 +101,8 @@ struct CommDevice {
     uint32_t nwin;
     uint32_t timeout_ms;
     uint32_t* status;             // host-mapped: [0] error code, [1] detail
-    uint32_t* scratch;            // [0] queue head, [1] CTAs done, [2..2+R) push counters
+    uint32_t* scratch;            // [0] queue head, [1] CTAs done, [2, 2+kMaxRanks) write counters,
+                                  // [2+kMaxRanks, 2+2*kMaxRanks) pull counters
 };
 
 // Per-launch arguments (passed by value as a __grid_constant__ kernel parameter).
@@ -100,10 +113,16 @@ struct LaunchArgs {
     uint64_t pipe_chunk;   // ring slot bytes
     uint64_t epoch;
     const CommDevice* comm;
-    const Post* posts;     // [R] my receive posts for this call (device copy)
+    const Post* posts;       // [R] my receive posts for this call (device copy)
+    const Post* send_posts;  // [R] my send posts for this call (device copy)
     uint32_t push_items[kMaxRanks];   // kPush items to receiver d (count toward done if zero copy)
     uint32_t fwd_items[kMaxRanks];    // kForward items into receiver d != me
-    uint64_t expect_done;             // bitmask of writers I must hear `done` from
+    uint32_t pull_items[kMaxRanks];   // kPull items from sender s
+    uint64_t recv_direct;             // senders with a direct flow into me
+    uint64_t recv_zc;                 // ... whose segment lands in a registered window of mine
+    uint64_t pull_req;                // ... from whom I asked to pull
+    uint64_t relay_writers;           // relays forwarding into me
+    uint64_t push_targets;            // receivers I have kPush items for
     uint64_t send_bytes[kMaxRanks];   // my outgoing pair sizes (checked against receivers' posts)
     const uint64_t* final_waits;      // pairs (ctrl byte offset of consumed flag, chunk index)
     uint32_t nfinal;

@@ -23,7 +23,10 @@
 //              or into the receiver's self ring when its buffer is unregistered;
 //   kStage   - relay hop 1: push into the staging ring hosted on the relay;
 //   kForward - relay hop 2 (or the receiver's drain of its self ring):
-//              staging slot -> final buffer.
+//              staging slot -> final buffer;
+//   kPull    - receiver-driven direct flow: TMA bulk loads straight out of the
+//              sender's registered send buffer over NVLink (an ingress-heavy
+//              receiver asks, a registered sender grants and skips its pushes).
 // Flags follow the reference's bounded-buffer recurrence
 // (proj/src/pipeline.cpp:97-106; device.cuh).  Waits are polled by the
 // producer thread with acquire loads and a global-timer timeout that raises an
@@ -155,6 +158,7 @@ enum EndAction : uint32_t {
     kActRelease1 = 1,  // st.release(flag1, tag1)
     kActRelease2 = 2,  // st.release(flag2, tag2)
     kActCount = 4,     // count a write into receiver count_d; publish done on the last
+    kActPulled = 8,    // count a pull from sender count_d; publish pulled on the last
 };
 
 struct StageDesc {
@@ -178,6 +182,8 @@ struct SharedState {
     StageDesc desc[kStages];
     uint64_t seg_base[kMaxRanks * kMaxRanks];  // (receiver, sender) -> resolved segment base
     uint32_t seg_mode[kMaxRanks * kMaxRanks];  // 0 = unresolved
+    uint64_t send_base[kMaxRanks];             // sender -> its registered send segment (pull)
+    uint32_t send_mode[kMaxRanks];             // 0 = unresolved
 };
 
 // Resolve receiver d's post for sender s (producer thread).
@@ -197,9 +203,30 @@ __device__ bool resolve(SharedState& sh, const LaunchArgs& a, int d, int s) {
             return false;
         }
     }
-    sh.seg_base[key] = mode == kPostZeroCopy ? c->win_table[win * kMaxRanks + d] + off : 0;
+    sh.seg_base[key] = (mode & 0xf) == kPostZeroCopy ? c->win_table[win * kMaxRanks + d] + off : 0;
     sh.seg_mode[key] = mode;
     return true;
+}
+
+// Sender s's send post for me (the receiver), cached per CTA.  False on timeout.
+__device__ bool resolve_send(SharedState& sh, const LaunchArgs& a, int s) {
+    if (sh.send_mode[s]) return true;
+    const CommDevice* c = a.comm;
+    const Post* p = reinterpret_cast<const CtrlHeader*>(c->ctrl[s])->send_post + c->rank;
+    if (!wait_ge(&p->tag, a.epoch, c, kErrPostTimeout)) return false;
+    const uint32_t mode = *reinterpret_cast<const volatile uint32_t*>(&p->mode);
+    const uint32_t win = *reinterpret_cast<const volatile uint32_t*>(&p->win);
+    const uint64_t off = *reinterpret_cast<const volatile uint64_t*>(&p->off);
+    sh.send_base[s] = mode == kSendRegistered ? c->win_table[win * kMaxRanks + s] + off : 0;
+    sh.send_mode[s] = mode;
+    return true;
+}
+
+// Does receiver d pull my segment instead of me pushing it?  (d asked, and
+// my send segment for d is registered.)  Needs d's receive post resolved.
+__device__ __forceinline__ bool pull_granted_to(const SharedState& sh, const LaunchArgs& a, int d) {
+    const int me = a.comm->rank;
+    return (sh.seg_mode[d * kMaxRanks + me] & kPostPullRequest) && a.send_posts[d].mode == kSendRegistered;
 }
 
 __device__ __forceinline__ uint8_t* ring_slot(const LaunchArgs& a, int host, int s, int d, uint32_t seq) {
@@ -212,9 +239,12 @@ __device__ __forceinline__ uint64_t* ctrl_flag(const LaunchArgs& a, int rank, ui
     return reinterpret_cast<uint64_t*>(a.comm->ctrl[rank] + off);
 }
 
-// Producer: the item's source, destination and end-of-item actions.  False
-// when the item must be skipped (a wait failed; the error is latched).
-__device__ bool prepare(SharedState& sh, const LaunchArgs& a, const Item& it, uint64_t& src, uint64_t& dst,
+enum Prep { kGo, kSkip };
+
+// Producer: the item's source, destination and end-of-item actions.  kSkip
+// when the item has nothing to do (pull granted / declined) or a wait failed
+// (the error is latched in the status word).
+__device__ Prep prepare(SharedState& sh, const LaunchArgs& a, const Item& it, uint64_t& src, uint64_t& dst,
                         StageDesc& end, bool& coherent) {
     const CommDevice* c = a.comm;
     const int me = c->rank, R = c->nranks;
@@ -222,36 +252,52 @@ __device__ bool prepare(SharedState& sh, const LaunchArgs& a, const Item& it, ui
     dst = it.dst;
     coherent = false;
     end.action = 0;
-    if (it.kind == kLocal) return true;
+    if (it.kind == kLocal) return kGo;
+    if (it.kind == kPull) {  // my direct flow from sender s, if s granted the pull
+        const int s = it.peer;
+        if (!resolve_send(sh, a, s)) return kSkip;
+        if (sh.send_mode[s] != kSendRegistered) return kSkip;  // declined: s pushes instead
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        src = sh.send_base[s] + it.src;
+        end.action = kActPulled;
+        end.count_d = s;
+        end.count_target = a.pull_items[s];
+        return kGo;
+    }
     if (it.kind == kPush || it.kind == kStage) {
         const int host = it.peer;  // receiver (push) or relay (stage)
         const int d = it.kind == kPush ? it.peer : it.aux;
         if (it.kind == kPush) {
-            if (!resolve(sh, a, d, me)) return false;
-            if (sh.seg_mode[d * kMaxRanks + me] == kPostZeroCopy) {
+            if (!resolve(sh, a, d, me)) return kSkip;
+            if (pull_granted_to(sh, a, d)) return kSkip;  // d pulls this range itself
+            if ((sh.seg_mode[d * kMaxRanks + me] & 0xf) == kPostZeroCopy) {
                 dst = sh.seg_base[d * kMaxRanks + me] + it.dst;
                 end.action = kActCount;
                 end.count_d = d;
                 end.count_target = a.fwd_items[d] + a.push_items[d];
-                return true;
+                return kGo;
             }
         }
         const uint32_t slot = it.seq % a.slots;
         if (it.seq >= a.slots &&
             !wait_ge(ctrl_flag(a, me, FlagLayout::consumed_off(R, d, host, slot)), tag_of(a.epoch, it.seq - a.slots), c,
                      kErrSlotTimeout))
-            return false;
+            return kSkip;
         dst = reinterpret_cast<uint64_t>(ring_slot(a, host, me, d, it.seq));
         end.action = kActRelease1;  // chunk landed in the slot: raise its ready flag
         end.flag1 = ctrl_flag(a, host, FlagLayout::ready_off(R, me, d, slot));
         end.tag1 = tag_of(a.epoch, it.seq);
-        return true;
+        return kGo;
     }
     // kForward: ring (s, d) hosted here -> receiver d
     const int s = it.aux, d = it.peer;
+    if (d == me && ((a.pull_req >> s) & 1)) {  // my self ring is idle if s granted my pull
+        if (!resolve_send(sh, a, s)) return kSkip;
+        if (sh.send_mode[s] == kSendRegistered) return kSkip;
+    }
     const uint32_t slot = it.seq % a.slots;
     if (!wait_ge(ctrl_flag(a, me, FlagLayout::ready_off(R, s, d, slot)), tag_of(a.epoch, it.seq), c, kErrReadyTimeout))
-        return false;
+        return kSkip;
     asm volatile("fence.proxy.async.global;" ::: "memory");  // peer-written slot, read by TMA
     coherent = true;
     src = reinterpret_cast<uint64_t>(ring_slot(a, me, s, d, it.seq));
@@ -260,23 +306,24 @@ __device__ bool prepare(SharedState& sh, const LaunchArgs& a, const Item& it, ui
     end.tag2 = tag_of(a.epoch, it.seq);
     if (d == me) {
         dst = a.posts[s].off + it.dst;  // staged self receive: absolute local address
-        return true;
+        return kGo;
     }
-    if (!resolve(sh, a, d, s)) return false;
-    if (sh.seg_mode[d * kMaxRanks + s] != kPostZeroCopy) {
+    if (!resolve(sh, a, d, s)) return kSkip;
+    if ((sh.seg_mode[d * kMaxRanks + s] & 0xf) != kPostZeroCopy) {
         atomicCAS(c->status, 0u, static_cast<uint32_t>(kErrRelayToStaged));
-        return false;
+        return kSkip;
     }
     dst = sh.seg_base[d * kMaxRanks + s] + it.dst;
     uint32_t target = a.fwd_items[d];
     if (a.push_items[d]) {  // my own pushes to d count only if d takes them in place
-        if (!resolve(sh, a, d, me)) return false;
-        if (sh.seg_mode[d * kMaxRanks + me] == kPostZeroCopy) target += a.push_items[d];
+        if (!resolve(sh, a, d, me)) return kSkip;
+        if ((sh.seg_mode[d * kMaxRanks + me] & 0xf) == kPostZeroCopy && !pull_granted_to(sh, a, d))
+            target += a.push_items[d];
     }
     end.action |= kActCount;
     end.count_d = d;
     end.count_target = target;
-    return true;
+    return kGo;
 }
 
 __device__ void produce(SharedState& sh, uint8_t* stages, const LaunchArgs& a) {
@@ -293,7 +340,7 @@ __device__ void produce(SharedState& sh, uint8_t* stages, const LaunchArgs& a) {
         uint64_t src, dst;
         StageDesc end{};
         bool coherent = false;
-        if (!prepare(sh, a, it, src, dst, end, coherent)) continue;
+        if (prepare(sh, a, it, src, dst, end, coherent) != kGo) continue;
         // head: bytes until the destination is 16-byte aligned
         uint64_t n = it.bytes;
         uint32_t head = static_cast<uint32_t>((16 - (dst & 15)) & 15);
@@ -410,6 +457,13 @@ __device__ void consume(SharedState& sh, const uint8_t* stages, const LaunchArgs
                         st_release(&h->done[a.comm->rank], a.epoch);
                     }
                 }
+                if (ds.action & kActPulled) {
+                    const uint32_t prev = atomicAdd(&counters[kMaxRanks + ds.count_d], 1u);
+                    if (prev + 1 == ds.count_target) {
+                        CtrlHeader* h = reinterpret_cast<CtrlHeader*>(a.comm->ctrl[ds.count_d]);
+                        st_release(&h->pulled[a.comm->rank], a.epoch);
+                    }
+                }
             }
         }
     }
@@ -430,6 +484,7 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
     const int me = c->rank, R = c->nranks;
 
     for (int i = tid; i < kMaxRanks * kMaxRanks; i += kThreads) sh.seg_mode[i] = 0;
+    for (int i = tid; i < kMaxRanks; i += kThreads) sh.send_mode[i] = 0;
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&sh.full[s], 1);
@@ -438,10 +493,13 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // Prologue: publish where each sender's segment lands in my buffer.
-    if (!a.local_only && blockIdx.x == 0 && tid < R) {
-        const Post p = a.posts[tid];
+    if (!a.local_only && blockIdx.x == 0 && tid < 2 * R) {
+        const bool send_side = tid >= R;
+        const int peer = send_side ? tid - R : tid;
+        const Post p = send_side ? a.send_posts[peer] : a.posts[peer];
         if (p.tag) {
-            Post* mine = reinterpret_cast<CtrlHeader*>(c->ctrl[me])->post + tid;
+            CtrlHeader* h = reinterpret_cast<CtrlHeader*>(c->ctrl[me]);
+            Post* mine = (send_side ? h->send_post : h->post) + peer;
             mine->win = p.win;
             mine->mode = p.mode;
             mine->off = p.off;
@@ -470,11 +528,29 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
                     wait_ge(reinterpret_cast<const uint64_t*>(c->ctrl[me] + a.final_waits[2 * i]),
                             tag_of(a.epoch, static_cast<uint32_t>(a.final_waits[2 * i + 1])), c, kErrFinalTimeout);
                 const CtrlHeader* h = reinterpret_cast<const CtrlHeader*>(c->ctrl[me]);
-                for (int w = 0; w < R; ++w)
-                    if ((a.expect_done >> w) & 1) wait_ge(&h->done[w], a.epoch, c, kErrDoneTimeout);
+                for (int w = 0; w < R; ++w) {
+                    if ((a.relay_writers >> w) & 1) wait_ge(&h->done[w], a.epoch, c, kErrDoneTimeout);
+                    if ((a.recv_direct >> w) & 1) {  // sender w pushed into my window unless I pulled
+                        bool pulled = false;
+                        if ((a.pull_req >> w) & 1) {
+                            const Post* sp = reinterpret_cast<const CtrlHeader*>(c->ctrl[w])->send_post + me;
+                            if (!wait_ge(&sp->tag, a.epoch, c, kErrPostTimeout)) continue;
+                            pulled = *reinterpret_cast<const volatile uint32_t*>(&sp->mode) == kSendRegistered;
+                        }
+                        if (!pulled && ((a.recv_zc >> w) & 1) && !((a.relay_writers >> w) & 1))
+                            wait_ge(&h->done[w], a.epoch, c, kErrDoneTimeout);
+                    }
+                    if ((a.push_targets >> w) & 1) {  // receiver w pulled my segment: wait until it has
+                        const Post* rp = reinterpret_cast<const CtrlHeader*>(c->ctrl[w])->post + me;
+                        if (!wait_ge(&rp->tag, a.epoch, c, kErrPostTimeout)) continue;
+                        const uint32_t mode = *reinterpret_cast<const volatile uint32_t*>(&rp->mode);
+                        if ((mode & kPostPullRequest) && a.send_posts[w].mode == kSendRegistered)
+                            wait_ge(&h->pulled[w], a.epoch, c, kErrDoneTimeout);
+                    }
+                }
             }
             uint32_t* counters = scratch + 2;
-            for (int d = 0; d < R; ++d) counters[d] = 0;
+            for (int d = 0; d < R; ++d) counters[d] = counters[kMaxRanks + d] = 0;
             scratch[0] = 0;
             __threadfence();
             scratch[1] = 0;

@@ -56,6 +56,7 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
     if (slots == 0 || slots > kMaxSlots) throw Error(nimbleInvalidArgument, "schedule: bad slot count");
     Schedule sc;
     sc.posts = rb.recv_post;
+    sc.send_posts = rb.send_post;
     std::vector<Keyed> keyed;
 
     // self segment: local copy
@@ -96,17 +97,29 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
                     const size_t first = keyed.size();
                     cut(keyed, proto, rb.send_ptr[d] + off, off, bytes, pipe_chunk, 0.0);
                     sc.push_items[d] += static_cast<uint32_t>(keyed.size() - first);
+                    sc.push_targets |= 1ull << d;
                     sc.moved_bytes += bytes;
                 }
                 if (d == me) {
-                    if (rb.recv_post[s].mode == kPostStaged) {  // drain my self ring (s, me)
+                    sc.recv_direct |= 1ull << s;
+                    if (rb.pull) {  // receiver-driven: used if the sender grants it at run time
+                        sc.pull_req |= 1ull << s;
+                        Item proto{};
+                        proto.kind = kPull;
+                        proto.peer = static_cast<uint8_t>(s);
+                        const size_t first = keyed.size();
+                        cut(keyed, proto, 1, rb.recv_ptr[s] + off, bytes, pipe_chunk, 0.0);
+                        for (size_t i = first; i < keyed.size(); ++i) keyed[i].item.src = off + static_cast<uint64_t>(keyed[i].item.seq) * pipe_chunk;
+                        sc.pull_items[s] += static_cast<uint32_t>(keyed.size() - first);
+                    }
+                    if ((rb.recv_post[s].mode & 0xf) == kPostStaged) {  // drain my self ring (s, me)
                         Item proto{};
                         proto.kind = kForward;
                         proto.peer = static_cast<uint8_t>(me);
                         proto.aux = static_cast<uint16_t>(s);
                         cut(keyed, proto, 0, off, bytes, pipe_chunk, kHop2);
                     } else {
-                        sc.expect_done |= 1ull << s;
+                        sc.recv_zc |= 1ull << s;
                     }
                 }
             } else {  // two-hop relay through GPU `via`
@@ -136,7 +149,7 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
                     cut(keyed, proto, 0, off, bytes, pipe_chunk, kHop2);
                     sc.fwd_items[d] += static_cast<uint32_t>(keyed.size() - first);
                 }
-                if (d == me) sc.expect_done |= 1ull << v;
+                if (d == me) sc.relay_writers |= 1ull << v;
             }
             off += bytes;
         }

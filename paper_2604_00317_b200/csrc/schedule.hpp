@@ -27,15 +27,19 @@ struct RankBuffers {
     std::vector<uint64_t> send_ptr, send_bytes;  // [R] my outgoing segments
     std::vector<uint64_t> recv_ptr, recv_bytes;  // [R] my incoming segments
     std::vector<Post> recv_post;                 // [R] mode/win/off per sender (tag != 0: present)
+    std::vector<Post> send_post;                 // [R] registered window of each outgoing segment
+    bool pull = false;                           // ask senders to let me pull my direct flows
 };
 
 struct Schedule {
     std::vector<Item> items;
     std::vector<Post> posts;
     std::vector<uint64_t> final_waits;  // (ctrl byte offset, chunk index) pairs
+    std::vector<Post> send_posts;
     uint32_t push_items[kMaxRanks] = {};
     uint32_t fwd_items[kMaxRanks] = {};
-    uint64_t expect_done = 0;
+    uint32_t pull_items[kMaxRanks] = {};
+    uint64_t recv_direct = 0, recv_zc = 0, pull_req = 0, relay_writers = 0, push_targets = 0;
     int relay_flows = 0;
     uint64_t moved_bytes = 0;  // my outgoing payload (incl. self segment)
 };

@@ -67,7 +67,7 @@ def _entry(fn, rank, world, port, q, args):
         q.put((rank, "ERROR " + traceback.format_exc()))
 
 
-def _exchange_and_check(comm, rank, R, m, register, seed):
+def _exchange_and_check(comm, rank, R, m, register, seed, register_send=False):
     from paper_2604_00317_b200 import comm as C
     sc, sd, rc, rd = C.packed_displs(m, R, rank)
     send = torch.empty(max(sum(sc), 16), dtype=torch.uint8, device="cuda")
@@ -75,6 +75,7 @@ def _exchange_and_check(comm, rank, R, m, register, seed):
     for d in range(R):
         C.fill_payload(send[sd[d]:], 0, sc[d], seed, rank, d)
     h = comm.register(recv) if register else None
+    hs = comm.register(send) if register_send else None
     comm.alltoallv(send, sc, sd, recv, rc, rd)
     torch.cuda.synchronize()
     comm.check_async()
@@ -86,6 +87,8 @@ def _exchange_and_check(comm, rank, R, m, register, seed):
     torch.cuda.synchronize()
     if h is not None:
         comm.deregister(h)
+    if hs is not None:
+        comm.deregister(hs)
     return int(bad.item()), tail_ok
 
 
@@ -93,6 +96,23 @@ def w_skewed(comm, rank, R, per_rank, ratio, register):
     from paper_2604_00317_b200 import planner as P
     m = P.gen_skewed_a2av(R, per_rank, ratio, 0)
     return _exchange_and_check(comm, rank, R, m, register, 11)
+
+
+def w_pull_modes(comm, rank, R):
+    """Receiver-driven pulls: every (pull mode, send registered, recv registered)
+    combination delivers bit-exactly (granted pulls, declined pulls falling back
+    to zero-copy or staged pushes)."""
+    from paper_2604_00317_b200 import planner as P
+    out = []
+    for pull in (0, 1, 2):
+        comm.set_config(pull=pull)
+        for reg_send in (True, False):
+            for reg_recv in (True, False):
+                for ratio in (0.9, 1.0 / (R - 1)):
+                    m = P.gen_skewed_a2av(R, 6 * MiB + 7, ratio, 1 % R)
+                    out.append(_exchange_and_check(comm, rank, R, m, reg_recv, 31, reg_send))
+    comm.set_config(pull=0)
+    return out
 
 
 def w_irregular(comm, rank, R):
@@ -109,9 +129,9 @@ def w_repeat_mixed(comm, rank, R):
     receive buffers and matrices (epochs, flag tags, schedule cache)."""
     from paper_2604_00317_b200 import planner as P
     res = []
-    for it in range(6):
+    for it in range(8):
         m = P.gen_skewed_a2av(R, (3 + it) * MiB + it, 0.3 + 0.1 * it, it % R)
-        res.append(_exchange_and_check(comm, rank, R, m, it % 2 == 0, 100 + it))
+        res.append(_exchange_and_check(comm, rank, R, m, it % 2 == 0, 100 + it, it % 4 < 2))
     return res
 
 
@@ -177,6 +197,13 @@ def test_skewed_alltoallv(per_rank, ratio, register):
     R = min(_ngpus(), 4)
     for r, (bad, tail_ok) in _spawn("w_skewed", R, per_rank, ratio, register).items():
         assert bad == 0 and tail_ok, r
+
+
+@need2
+def test_pull_modes_all_registration_combinations():
+    R = min(_ngpus(), 4)
+    for r, res in _spawn("w_pull_modes", R).items():
+        assert all(bad == 0 and ok for bad, ok in res), (r, res)
 
 
 @need2
