@@ -183,10 +183,11 @@ typedef struct {
     uint64_t p2p_buffer;          /* staging bytes per ring, 10 MiB (pipeline.hpp:18)   */
     int channels_per_peer;        /* rings per relayed flow, 1 (pipeline.hpp:23)        */
     int ctas;                     /* forwarding-engine CTAs per launch, 0 = auto        */
-    uint64_t direct_chunk;        /* work-item size for local copies, 0 = auto          */
-    int pull;                     /* receiver-driven pulls: 0 = auto (a rank whose ingress
-                                     exceeds its egress pulls from registered senders),
-                                     1 = never, 2 = always when the sender is registered */
+    uint64_t direct_chunk;        /* work-item size of direct pushes/pulls, self rings and
+                                     local copies (<= pipe_chunk), 0 = auto (128 KiB)      */
+    int pull;                     /* receiver-driven pulls: 2 = always when the sender's
+                                     segment is registered (default), 1 = never (push),
+                                     0 = auto (only ranks with ingress > 1.25 x egress) */
 } nimbleCommConfig;
 
 nimbleResult_t nimbleCommConfigDefault(nimbleCommConfig* cfg);
@@ -272,6 +273,11 @@ nimbleResult_t nimbleBenchMatrix(nimbleComm_t comm, const uint64_t* matrix, int 
  * Exercises the bootstrap that nimbleCommInitRank uses, without a GPU. */
 nimbleResult_t nimbleBootstrapAllgather(const nimbleUniqueId* id, int rank, int nranks, const void* in, size_t n,
                                         void* out);
+
+/* Device timeline of the comm's last launch (%globaltimer ns): kernel start,
+ * prologue done, first item, last item, CTAs done, completions signalled,
+ * completions observed.  Needs NIMBLE_TRACE=1 at comm creation; n >= 8. */
+nimbleResult_t nimbleCommDebugTrace(nimbleComm_t comm, uint64_t* out, int n);
 
 #ifdef __cplusplus
 }

@@ -114,6 +114,7 @@ SIGNATURES = {
     "nimbleBenchSkewed": [c_void_p, c_u64, c_double, c_int, c_int, c_int, P(BenchResult)],
     "nimbleBenchMatrix": [c_void_p, P(c_u64), c_int, c_int, P(BenchResult)],
     "nimbleBootstrapAllgather": [P(UniqueId), c_int, c_int, c_void_p, c_size, c_void_p],
+    "nimbleCommDebugTrace": [c_void_p, P(c_u64), c_int],
 }
 _RESTYPES = {"nimbleGetErrorString": c_char_p, "nimbleGetLastError": c_char_p}
 

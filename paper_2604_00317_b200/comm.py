@@ -105,6 +105,12 @@ class Comm:
         if e:
             raise _lib.NimbleError(e, _lib.lib().nimbleGetLastError().decode())
 
+    def debug_trace(self):
+        """Device timeline (ns) of the last launch; needs NIMBLE_TRACE=1."""
+        out = (c_u64 * 8)()
+        _lib.call("nimbleCommDebugTrace", self._h, out, 8)
+        return list(out)
+
     # -- registration
     def register(self, tensor, nbytes=None):
         h = c_void_p()

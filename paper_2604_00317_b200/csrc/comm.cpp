@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <list>
 #include <map>
@@ -236,6 +237,7 @@ struct nimbleComm {
     std::list<nb::CachedPlan> plans;
     std::list<nb::CachedSchedule> schedules;
     cudaStream_t bench_stream = nullptr;
+    uint64_t* d_trace = nullptr;  // NIMBLE_TRACE=1: device timeline of the last launch
 };
 
 namespace nb {
@@ -262,6 +264,7 @@ void upload_view(nimbleComm* c) {
 }
 
 constexpr uint32_t kMaxWindows = 256;
+constexpr uint64_t kDefaultDirectChunk = 128ull << 10;
 
 uint32_t slot_count(const nimbleCommConfig& cfg) {
     if (cfg.pipe_chunk == 0) throw Error(nimbleInvalidArgument, "config: pipe_chunk must be positive");
@@ -286,7 +289,7 @@ void default_config(nimbleCommConfig* cfg, int nranks) {
     cfg->channels_per_peer = 1;
     cfg->ctas = 0;
     cfg->direct_chunk = 0;
-    cfg->pull = 0;
+    cfg->pull = 2;
 }
 
 // Allocate ctrl + staging, exchange handles / pointers, map peers.
@@ -337,6 +340,8 @@ void setup_common(nimbleComm* c) {
     std::memset(c->h_status, 0, 64);
     CUDA_TRY(cudaHostGetDevicePointer(&c->d_status, c->h_status, 0));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->bench_stream, cudaStreamNonBlocking));
+    if (const char* t = std::getenv("NIMBLE_TRACE"); t && *t == '1')
+        CUDA_TRY(cudaMalloc(&c->d_trace, sizeof(uint64_t) * kTraceSlots));
     c->win_table.assign(static_cast<size_t>(kMaxWindows) * kMaxRanks, 0);
 }
 
@@ -456,7 +461,9 @@ void fill_posts(nimbleComm* c, RankBuffers& rb) {
     uint64_t ingress = 0, egress = 0;
     for (int p = 0; p < rb.R; ++p)
         if (p != rb.me) ingress += rb.recv_bytes[p], egress += rb.send_bytes[p];
-    rb.pull = c->cfg.pull == 2 || (c->cfg.pull == 0 && ingress > egress);
+    // auto: only a clearly ingress-heavy rank pulls; measured on 4xB200, mixing
+    // push and pull on one port costs more than it saves, so the default is 2
+    rb.pull = c->cfg.pull == 2 || (c->cfg.pull == 0 && ingress > egress + egress / 4);
     rb.send_post.assign(static_cast<size_t>(rb.R), Post{});
     for (int d = 0; d < rb.R; ++d) {
         if (d == rb.me || rb.send_bytes[d] == 0) continue;
@@ -512,8 +519,11 @@ CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& 
         }
     CachedSchedule cs;
     cs.key = key;
-    const uint64_t local_chunk = c->cfg.direct_chunk ? c->cfg.direct_chunk : (1ull << 20);
-    cs.sc = build_schedule(plan, rb, c->cfg.pipe_chunk, slot_count(c->cfg), local_chunk);
+    const char* env = std::getenv("NIMBLE_DIRECT_CHUNK");
+    const uint64_t dchunk = c->cfg.direct_chunk ? c->cfg.direct_chunk
+                            : env && *env          ? std::strtoull(env, nullptr, 0)
+                                                   : kDefaultDirectChunk;
+    cs.sc = build_schedule(plan, rb, c->cfg.pipe_chunk, slot_count(c->cfg), dchunk);
     if (c->schedules.size() >= 4) {  // recycle the oldest entry's device buffers
         CUDA_TRY(cudaDeviceSynchronize());  // no launch may still read them
         CachedSchedule& old = c->schedules.back();
@@ -552,9 +562,15 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     a.pull_req = cs.sc.pull_req;
     a.relay_writers = cs.sc.relay_writers;
     a.push_targets = cs.sc.push_targets;
+    a.write_targets = cs.sc.write_targets;
     a.final_waits = cs.finals.p;
     a.nfinal = static_cast<uint32_t>(cs.sc.final_waits.size() / 2);
     a.local_only = 0;
+    if (c->d_trace) {
+        static const uint64_t init[kTraceSlots] = {~0ull, 0, ~0ull, 0, 0, 0, 0, 0};
+        CUDA_TRY(cudaMemcpyAsync(c->d_trace, init, sizeof init, cudaMemcpyHostToDevice, st));
+        a.trace = c->d_trace;
+    }
     int ctas = c->cfg.ctas > 0 ? c->cfg.ctas : c->sms;
     ctas = std::max(1, std::min(ctas, c->sms));
     // every rank launches even with nothing to move: its posts and done
@@ -899,6 +915,7 @@ nimbleResult_t nimbleCommDestroy(nimbleComm_t c) {
             cudaFree(c->d_view);
             cudaFree(c->d_win_table);
             cudaFree(c->d_scratch);
+            if (c->d_trace) cudaFree(c->d_trace);
             cudaFreeHost(c->h_status);
             if (c->bench_stream) cudaStreamDestroy(c->bench_stream);
         }
@@ -1113,6 +1130,16 @@ nimbleResult_t nimbleBenchSkewed(nimbleComm_t c, uint64_t per_rank, double ratio
         if (!c) throw nb::Error(nimbleInvalidArgument, "bench: null comm");
         nb::Demand d = nb::demand_skewed(c->nranks, per_rank, ratio, hot, false);
         nb::bench_matrix(c, d.bytes, warmup, iters, out);
+    });
+}
+
+nimbleResult_t nimbleCommDebugTrace(nimbleComm_t c, uint64_t* out, int n) {
+    return guarded([&] {
+        if (!c || !out || n < nb::kTraceSlots) throw nb::Error(nimbleInvalidArgument, "trace: bad argument");
+        if (!c->d_trace) throw nb::Error(nimbleInvalidUsage, "trace: set NIMBLE_TRACE=1 before creating the comm");
+        nb::DeviceGuard g(c->device);
+        CUDA_TRY(cudaDeviceSynchronize());
+        CUDA_TRY(cudaMemcpy(out, c->d_trace, sizeof(uint64_t) * nb::kTraceSlots, cudaMemcpyDeviceToHost));
     });
 }
 

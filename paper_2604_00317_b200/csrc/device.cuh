@@ -123,10 +123,24 @@ struct LaunchArgs {
     uint64_t pull_req;                // ... from whom I asked to pull
     uint64_t relay_writers;           // relays forwarding into me
     uint64_t push_targets;            // receivers I have kPush items for
+    uint64_t write_targets;           // peers whose memory I may write (pushes, relay forwards)
     uint64_t send_bytes[kMaxRanks];   // my outgoing pair sizes (checked against receivers' posts)
     const uint64_t* final_waits;      // pairs (ctrl byte offset of consumed flag, chunk index)
     uint32_t nfinal;
     uint32_t local_only;              // 1: flagless single-GPU exchange (no ctrl)
+    uint64_t* trace;                  // optional globaltimer stamps (NIMBLE_TRACE=1), see kTrace*
+};
+
+// Device timeline of one launch (ns, %globaltimer): written when tracing is on.
+enum TraceSlot : int {
+    kTraceKernelStart = 0,   // min over CTAs: entered the kernel
+    kTracePrologueDone = 1,  // CTA 0: posts published
+    kTraceFirstItem = 2,     // min over CTAs: first item prepared
+    kTraceLastItem = 3,      // max over CTAs: producer out of items
+    kTraceCtasDone = 4,      // last CTA arrived at the epilogue
+    kTraceSignalled = 5,     // done / pulled published
+    kTraceWaited = 6,        // all incoming completions observed
+    kTraceSlots = 8,
 };
 
 }  // namespace nb

@@ -63,6 +63,10 @@ __device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ uint64_t global_ns() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -157,8 +161,6 @@ enum StageFlags : uint32_t {
 enum EndAction : uint32_t {
     kActRelease1 = 1,  // st.release(flag1, tag1)
     kActRelease2 = 2,  // st.release(flag2, tag2)
-    kActCount = 4,     // count a write into receiver count_d; publish done on the last
-    kActPulled = 8,    // count a pull from sender count_d; publish pulled on the last
 };
 
 struct StageDesc {
@@ -173,7 +175,6 @@ struct StageDesc {
     uint64_t tag1;
     uint64_t* flag2;
     uint64_t tag2;
-    uint32_t count_d, count_target;
 };
 
 struct SharedState {
@@ -219,6 +220,7 @@ __device__ bool resolve_send(SharedState& sh, const LaunchArgs& a, int s) {
     const uint64_t off = *reinterpret_cast<const volatile uint64_t*>(&p->off);
     sh.send_base[s] = mode == kSendRegistered ? c->win_table[win * kMaxRanks + s] + off : 0;
     sh.send_mode[s] = mode;
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // generic -> async proxy (TMA reads)
     return true;
 }
 
@@ -257,11 +259,7 @@ __device__ Prep prepare(SharedState& sh, const LaunchArgs& a, const Item& it, ui
         const int s = it.peer;
         if (!resolve_send(sh, a, s)) return kSkip;
         if (sh.send_mode[s] != kSendRegistered) return kSkip;  // declined: s pushes instead
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        src = sh.send_base[s] + it.src;
-        end.action = kActPulled;
-        end.count_d = s;
-        end.count_target = a.pull_items[s];
+        src = sh.send_base[s] + it.src;  // pulled[] is raised once per launch (epilogue)
         return kGo;
     }
     if (it.kind == kPush || it.kind == kStage) {
@@ -271,10 +269,7 @@ __device__ Prep prepare(SharedState& sh, const LaunchArgs& a, const Item& it, ui
             if (!resolve(sh, a, d, me)) return kSkip;
             if (pull_granted_to(sh, a, d)) return kSkip;  // d pulls this range itself
             if ((sh.seg_mode[d * kMaxRanks + me] & 0xf) == kPostZeroCopy) {
-                dst = sh.seg_base[d * kMaxRanks + me] + it.dst;
-                end.action = kActCount;
-                end.count_d = d;
-                end.count_target = a.fwd_items[d] + a.push_items[d];
+                dst = sh.seg_base[d * kMaxRanks + me] + it.dst;  // done[] is raised once per launch
                 return kGo;
             }
         }
@@ -314,21 +309,20 @@ __device__ Prep prepare(SharedState& sh, const LaunchArgs& a, const Item& it, ui
         return kSkip;
     }
     dst = sh.seg_base[d * kMaxRanks + s] + it.dst;
-    uint32_t target = a.fwd_items[d];
-    if (a.push_items[d]) {  // my own pushes to d count only if d takes them in place
-        if (!resolve(sh, a, d, me)) return kSkip;
-        if ((sh.seg_mode[d * kMaxRanks + me] & 0xf) == kPostZeroCopy && !pull_granted_to(sh, a, d))
-            target += a.push_items[d];
-    }
-    end.action |= kActCount;
-    end.count_d = d;
-    end.count_target = target;
     return kGo;
+}
+
+__device__ __forceinline__ void trace_min(const LaunchArgs& a, int slot) {
+    if (a.trace) atomicMin(reinterpret_cast<unsigned long long*>(a.trace + slot), global_ns());
+}
+__device__ __forceinline__ void trace_max(const LaunchArgs& a, int slot) {
+    if (a.trace) atomicMax(reinterpret_cast<unsigned long long*>(a.trace + slot), global_ns());
 }
 
 __device__ void produce(SharedState& sh, uint8_t* stages, const LaunchArgs& a) {
     uint32_t* scratch = a.comm->scratch;
     uint32_t cnt = 0;
+    bool first = true;
     auto next_slot = [&](uint32_t& slot) {
         slot = cnt % kStages;
         if (cnt >= kStages) mbar_wait(&sh.empty[slot], ((cnt / kStages) - 1) & 1);
@@ -341,6 +335,10 @@ __device__ void produce(SharedState& sh, uint8_t* stages, const LaunchArgs& a) {
         StageDesc end{};
         bool coherent = false;
         if (prepare(sh, a, it, src, dst, end, coherent) != kGo) continue;
+        if (first) {
+            trace_min(a, kTraceFirstItem);
+            first = false;
+        }
         // head: bytes until the destination is 16-byte aligned
         uint64_t n = it.bytes;
         uint32_t head = static_cast<uint32_t>((16 - (dst & 15)) & 15);
@@ -376,8 +374,6 @@ __device__ void produce(SharedState& sh, uint8_t* stages, const LaunchArgs& a) {
                 ds.tag1 = end.tag1;
                 ds.flag2 = end.flag2;
                 ds.tag2 = end.tag2;
-                ds.count_d = end.count_d;
-                ds.count_target = end.count_target;
             }
             uint32_t bytes = 0;
             if (nvec) {
@@ -395,6 +391,7 @@ __device__ void produce(SharedState& sh, uint8_t* stages, const LaunchArgs& a) {
             ++cnt;
         }
     }
+    trace_max(a, kTraceLastItem);
     uint32_t slot;
     next_slot(slot);
     sh.desc[slot].flags = kTerminate;
@@ -418,7 +415,7 @@ __device__ __forceinline__ void realign_store(const uint4* buf, uint8_t* out, ui
 __device__ void consume(SharedState& sh, const uint8_t* stages, const LaunchArgs& a) {
     const int ct = threadIdx.x - 32;  // consumer thread index
     const int lane = threadIdx.x & 31;
-    uint32_t* counters = a.comm->scratch + 2;
+    (void)a;
     for (uint32_t cnt = 0;; ++cnt) {
         const uint32_t slot = cnt % kStages;
         mbar_wait(&sh.full[slot], (cnt / kStages) & 1);
@@ -445,25 +442,11 @@ __device__ void consume(SharedState& sh, const uint8_t* stages, const LaunchArgs
             if (ct >= 32 && ct < 32 + static_cast<int>(ds.tail_n))
                 reinterpret_cast<uint8_t*>(ds.tail_dst)[ct - 32] =
                     ld_byte(reinterpret_cast<const uint8_t*>(ds.tail_src) + (ct - 32), coh);
-            asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+            if (ds.action) asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
             if (ct == 0 && ds.action) {
                 __threadfence_system();
                 if (ds.action & kActRelease1) st_release(ds.flag1, ds.tag1);
                 if (ds.action & kActRelease2) st_release(ds.flag2, ds.tag2);
-                if (ds.action & kActCount) {
-                    const uint32_t prev = atomicAdd(&counters[ds.count_d], 1u);
-                    if (prev + 1 == ds.count_target) {
-                        CtrlHeader* h = reinterpret_cast<CtrlHeader*>(a.comm->ctrl[ds.count_d]);
-                        st_release(&h->done[a.comm->rank], a.epoch);
-                    }
-                }
-                if (ds.action & kActPulled) {
-                    const uint32_t prev = atomicAdd(&counters[kMaxRanks + ds.count_d], 1u);
-                    if (prev + 1 == ds.count_target) {
-                        CtrlHeader* h = reinterpret_cast<CtrlHeader*>(a.comm->ctrl[ds.count_d]);
-                        st_release(&h->pulled[a.comm->rank], a.epoch);
-                    }
-                }
             }
         }
     }
@@ -483,6 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
     uint32_t* scratch = c->scratch;
     const int me = c->rank, R = c->nranks;
 
+    if (tid == 0) trace_min(a, kTraceKernelStart);
     for (int i = tid; i < kMaxRanks * kMaxRanks; i += kThreads) sh.seg_mode[i] = 0;
     for (int i = tid; i < kMaxRanks; i += kThreads) sh.send_mode[i] = 0;
     if (tid == 0) {
@@ -508,6 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
         }
     }
     __syncthreads();
+    if (tid == 0 && blockIdx.x == 0) trace_max(a, kTracePrologueDone);
 
     if (tid < 32) {
         if (tid == 0) produce(sh, stages, a);
@@ -516,41 +501,58 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
     }
     __syncthreads();
 
-    // Epilogue: the last CTA out waits for (a) my relayed chunks to be drained
-    // from their rings, (b) every writer into my buffer to report done; then
-    // resets the per-launch scratch for the next stream-ordered launch.
+    // Epilogue: the last CTA out publishes this rank's completions and waits
+    // for everyone else's -- one warp, lane p handling peer p, so the remote
+    // reads and waits run in parallel.  Then it resets the per-launch scratch
+    // for the next stream-ordered launch.
+    __shared__ uint32_t last_cta;
     if (tid == 0) {
-        __threadfence();
-        const uint32_t arrived = atomicAdd(&scratch[1], 1u);
-        if (arrived + 1 == gridDim.x) {
-            if (!a.local_only) {
-                for (uint32_t i = 0; i < a.nfinal; ++i)
-                    wait_ge(reinterpret_cast<const uint64_t*>(c->ctrl[me] + a.final_waits[2 * i]),
-                            tag_of(a.epoch, static_cast<uint32_t>(a.final_waits[2 * i + 1])), c, kErrFinalTimeout);
+        __threadfence_system();  // this CTA's peer writes, before the rank-wide completion count
+        last_cta = atomicAdd(&scratch[1], 1u) + 1 == gridDim.x;
+    }
+    __syncthreads();
+    if (last_cta && tid < 32) {
+        const int lane = tid;
+        if (lane == 0) trace_max(a, kTraceCtasDone);
+        if (!a.local_only) {
+            asm volatile("fence.acq_rel.sys;" ::: "memory");  // warp-wide: all CTAs' writes -> flags
+            if (lane < R) {
+                CtrlHeader* ph = reinterpret_cast<CtrlHeader*>(c->ctrl[lane]);
+                if ((a.write_targets >> lane) & 1) st_relaxed(&ph->done[me], a.epoch);
+                if ((a.pull_req >> lane) & 1) st_relaxed(&ph->pulled[me], a.epoch);
+            }
+            __syncwarp();
+            if (lane == 0) trace_max(a, kTraceSignalled);
+            for (uint32_t i = lane; i < a.nfinal; i += 32)  // relayed chunks drained from their rings
+                wait_ge(reinterpret_cast<const uint64_t*>(c->ctrl[me] + a.final_waits[2 * i]),
+                        tag_of(a.epoch, static_cast<uint32_t>(a.final_waits[2 * i + 1])), c, kErrFinalTimeout);
+            if (lane < R) {
+                const int w = lane;
                 const CtrlHeader* h = reinterpret_cast<const CtrlHeader*>(c->ctrl[me]);
-                for (int w = 0; w < R; ++w) {
-                    if ((a.relay_writers >> w) & 1) wait_ge(&h->done[w], a.epoch, c, kErrDoneTimeout);
-                    if ((a.recv_direct >> w) & 1) {  // sender w pushed into my window unless I pulled
-                        bool pulled = false;
-                        if ((a.pull_req >> w) & 1) {
-                            const Post* sp = reinterpret_cast<const CtrlHeader*>(c->ctrl[w])->send_post + me;
-                            if (!wait_ge(&sp->tag, a.epoch, c, kErrPostTimeout)) continue;
+                bool need_done = (a.relay_writers >> w) & 1;
+                if (((a.recv_direct >> w) & 1) && ((a.recv_zc >> w) & 1)) {  // w pushed in place unless I pulled
+                    bool pulled = false;
+                    if ((a.pull_req >> w) & 1) {
+                        const Post* sp = reinterpret_cast<const CtrlHeader*>(c->ctrl[w])->send_post + me;
+                        if (wait_ge(&sp->tag, a.epoch, c, kErrPostTimeout))
                             pulled = *reinterpret_cast<const volatile uint32_t*>(&sp->mode) == kSendRegistered;
-                        }
-                        if (!pulled && ((a.recv_zc >> w) & 1) && !((a.relay_writers >> w) & 1))
-                            wait_ge(&h->done[w], a.epoch, c, kErrDoneTimeout);
                     }
-                    if ((a.push_targets >> w) & 1) {  // receiver w pulled my segment: wait until it has
-                        const Post* rp = reinterpret_cast<const CtrlHeader*>(c->ctrl[w])->post + me;
-                        if (!wait_ge(&rp->tag, a.epoch, c, kErrPostTimeout)) continue;
+                    need_done |= !pulled;
+                }
+                if (need_done) wait_ge(&h->done[w], a.epoch, c, kErrDoneTimeout);
+                if ((a.push_targets >> w) & 1) {  // receiver w pulled my segment: wait until it has
+                    const Post* rp = reinterpret_cast<const CtrlHeader*>(c->ctrl[w])->post + me;
+                    if (wait_ge(&rp->tag, a.epoch, c, kErrPostTimeout)) {
                         const uint32_t mode = *reinterpret_cast<const volatile uint32_t*>(&rp->mode);
                         if ((mode & kPostPullRequest) && a.send_posts[w].mode == kSendRegistered)
                             wait_ge(&h->pulled[w], a.epoch, c, kErrDoneTimeout);
                     }
                 }
             }
-            uint32_t* counters = scratch + 2;
-            for (int d = 0; d < R; ++d) counters[d] = counters[kMaxRanks + d] = 0;
+            __syncwarp();
+        }
+        if (lane == 0) {
+            trace_max(a, kTraceWaited);
             scratch[0] = 0;
             __threadfence();
             scratch[1] = 0;

@@ -49,11 +49,12 @@ constexpr double kHop2 = 1e-9;  // forward of chunk k sorts right after its stag
 }  // namespace
 
 Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t pipe_chunk, uint32_t slots,
-                        uint64_t local_chunk) {
+                        uint64_t direct_chunk) {
     const int R = rb.R, me = rb.me;
     if (R > kMaxRanks) throw Error(nimbleInvalidArgument, "schedule: too many ranks");
     if (pipe_chunk == 0 || pipe_chunk > 0xffffffffull) throw Error(nimbleInvalidArgument, "schedule: bad pipe_chunk");
     if (slots == 0 || slots > kMaxSlots) throw Error(nimbleInvalidArgument, "schedule: bad slot count");
+    const uint64_t dchunk = std::min<uint64_t>(std::max<uint64_t>(direct_chunk, 4096), pipe_chunk);
     Schedule sc;
     sc.posts = rb.recv_post;
     sc.send_posts = rb.send_post;
@@ -66,7 +67,7 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
         Item proto{};
         proto.kind = kLocal;
         proto.peer = static_cast<uint8_t>(me);
-        cut(keyed, proto, rb.send_ptr[me], rb.recv_ptr[me], rb.send_bytes[me], std::max<uint64_t>(local_chunk, 1), 0.0);
+        cut(keyed, proto, rb.send_ptr[me], rb.recv_ptr[me], rb.send_bytes[me], dchunk, 0.0);
         sc.moved_bytes += rb.send_bytes[me];
     }
 
@@ -95,9 +96,10 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
                     proto.kind = kPush;
                     proto.peer = static_cast<uint8_t>(d);
                     const size_t first = keyed.size();
-                    cut(keyed, proto, rb.send_ptr[d] + off, off, bytes, pipe_chunk, 0.0);
+                    cut(keyed, proto, rb.send_ptr[d] + off, off, bytes, dchunk, 0.0);
                     sc.push_items[d] += static_cast<uint32_t>(keyed.size() - first);
                     sc.push_targets |= 1ull << d;
+                    sc.write_targets |= 1ull << d;
                     sc.moved_bytes += bytes;
                 }
                 if (d == me) {
@@ -108,8 +110,8 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
                         proto.kind = kPull;
                         proto.peer = static_cast<uint8_t>(s);
                         const size_t first = keyed.size();
-                        cut(keyed, proto, 1, rb.recv_ptr[s] + off, bytes, pipe_chunk, 0.0);
-                        for (size_t i = first; i < keyed.size(); ++i) keyed[i].item.src = off + static_cast<uint64_t>(keyed[i].item.seq) * pipe_chunk;
+                        cut(keyed, proto, 1, rb.recv_ptr[s] + off, bytes, dchunk, 0.0);
+                        for (size_t i = first; i < keyed.size(); ++i) keyed[i].item.src = off + static_cast<uint64_t>(keyed[i].item.seq) * dchunk;
                         sc.pull_items[s] += static_cast<uint32_t>(keyed.size() - first);
                     }
                     if ((rb.recv_post[s].mode & 0xf) == kPostStaged) {  // drain my self ring (s, me)
@@ -117,7 +119,7 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
                         proto.kind = kForward;
                         proto.peer = static_cast<uint8_t>(me);
                         proto.aux = static_cast<uint16_t>(s);
-                        cut(keyed, proto, 0, off, bytes, pipe_chunk, kHop2);
+                        cut(keyed, proto, 0, off, bytes, dchunk, kHop2);
                     } else {
                         sc.recv_zc |= 1ull << s;
                     }
@@ -148,6 +150,7 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
                     const size_t first = keyed.size();
                     cut(keyed, proto, 0, off, bytes, pipe_chunk, kHop2);
                     sc.fwd_items[d] += static_cast<uint32_t>(keyed.size() - first);
+                    sc.write_targets |= 1ull << d;
                 }
                 if (d == me) sc.relay_writers |= 1ull << v;
             }

@@ -39,13 +39,17 @@ struct Schedule {
     uint32_t push_items[kMaxRanks] = {};
     uint32_t fwd_items[kMaxRanks] = {};
     uint32_t pull_items[kMaxRanks] = {};
-    uint64_t recv_direct = 0, recv_zc = 0, pull_req = 0, relay_writers = 0, push_targets = 0;
+    uint64_t recv_direct = 0, recv_zc = 0, pull_req = 0, relay_writers = 0, push_targets = 0, write_targets = 0;
     int relay_flows = 0;
     uint64_t moved_bytes = 0;  // my outgoing payload (incl. self segment)
 };
 
+// pipe_chunk: relay ring chunk (reference staging geometry); direct_chunk:
+// work-item size of direct pushes / pulls / self-ring chunks (<= pipe_chunk)
+// and of local copies -- small enough that the last wave of items ends within
+// a few microseconds across CTAs.
 Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t pipe_chunk, uint32_t slots,
-                        uint64_t local_chunk);
+                        uint64_t direct_chunk);
 
 // 1-GPU emulated exchange: every pair's segment as local copies (packed layout).
 std::vector<Item> build_local_items(int R, const uint64_t* matrix, const uint64_t* send_base,

@@ -1,0 +1,52 @@
+"""Device timeline of one exchange on every rank (development aid; torchrun, NIMBLE_TRACE=1)."""
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2604_00317_b200 import comm as C  # noqa: E402
+from paper_2604_00317_b200 import planner as P  # noqa: E402
+
+MiB = 1 << 20
+NAMES = ["start", "prolog", "first", "last", "ctas", "signal", "waited"]
+
+
+def main():
+    os.environ["NIMBLE_TRACE"] = "1"
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+    dist.init_process_group("gloo")
+    uid = [C.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, 0)
+    comm = C.Comm.init_rank(world, uid[0], rank)
+    R = world
+    for pull in (1, 2):
+        comm.set_config(pull=pull)
+        for mib in (1, 256):
+            m = P.gen_skewed_a2av(R, mib * MiB, 0.7, 0)
+            sc, sd, rc, rd = C.packed_displs(m, R, rank)
+            send = torch.empty(max(sum(sc), 16), dtype=torch.uint8, device="cuda")
+            recv = torch.empty(max(sum(rc), 16), dtype=torch.uint8, device="cuda")
+            hs, hr = comm.register(send), comm.register(recv)
+            for _ in range(5):
+                comm.alltoallv(send, sc, sd, recv, rc, rd)
+            tr = comm.debug_trace()
+            allt = [None] * world
+            dist.all_gather_object(allt, tr)
+            if rank == 0:
+                t0 = min(t[0] for t in allt)
+                print(f"pull={pull} {mib}MiB (us from earliest kernel start; globaltimers assumed aligned)")
+                for r, t in enumerate(allt):
+                    print(f"  rank {r}: " + " ".join(f"{n}={(v - t0) / 1e3:8.1f}" for n, v in zip(NAMES, t[:7])),
+                          flush=True)
+            comm.deregister(hs)
+            comm.deregister(hr)
+    dist.barrier()
+    comm.destroy()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
