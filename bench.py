@@ -370,6 +370,7 @@ def run_multi(args):
 
     nccl = None
     if not args.no_baselines:
+        os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line
         pg = dist.new_group(backend="nccl")
         out = torch.empty_like(recv)
         ins, outs = list(sc), list(rc)
@@ -469,6 +470,11 @@ def run_reference(args):
 
 
 def main():
+    os.environ["NCCL_DEBUG"] = "WARN"
+    # The contract is ONE JSON line on stdout: everything else (NCCL's banner,
+    # C-level prints) goes to stderr; the line is written to the saved fd.
+    json_out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -490,7 +496,8 @@ def main():
     else:
         line = run_local(args)
     if line is not None:
-        print(json.dumps(line), flush=True)
+        json_out.write(json.dumps(line) + "\n")
+        json_out.flush()
 
 
 if __name__ == "__main__":

@@ -1,0 +1,133 @@
+"""BASELINE.json config sweeps on real GPUs (torchrun, one process per GPU).
+
+For the world size it is launched with (W), rank 0 prints one JSON line per
+point: nimble GB/s, fraction of the MCF port bound, NCCL all_to_all_single on
+the same buffers, relay flows, delivery mismatches.
+  c3  skewed all-to-allv, 256 MiB/rank, hotspot ratio 0.0 .. 0.9
+  c5  uniform all-to-allv (ratio 1/(W-1)), 256 MiB/rank
+  c4  irregular seeded matrix (seed 1, sparsity 0.5), total 1 KiB .. 1 GiB
+  c1  p2p 64 MiB 0 -> 1 (W = 3: one relay GPU under the mesh model)
+  c2  p2p 1 GiB 0 -> 1 (W = 4: two relay GPUs under the mesh model)
+SWEEP_CASES selects (default all that fit W).
+"""
+import json
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2604_00317_b200 import comm as C  # noqa: E402
+from paper_2604_00317_b200 import planner as P  # noqa: E402
+
+MiB = 1 << 20
+
+
+def max_over(x):
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def port_bound(m, R):
+    return max(max(sum(m[v * R + d] for d in range(R) if d != v), sum(m[s * R + v] for s in range(R) if s != v))
+               for v in range(R)) / 900e9
+
+
+def run_point(comm, pg, rank, R, m, name, fabric="nvswitch", iters=10, warmup=3, nccl=True, extra=None):
+    comm.set_config(fabric=fabric, gpus_per_node=R)
+    sc, sd, rc, rd = C.packed_displs(m, R, rank)
+    send = torch.empty(max(sum(sc), 16), dtype=torch.uint8, device="cuda")
+    recv = torch.zeros(max(sum(rc), 16), dtype=torch.uint8, device="cuda")
+    for d in range(R):
+        C.fill_payload(send[sd[d]:], 0, sc[d], 9, rank, d)
+    hs, hr = comm.register(send), comm.register(recv)
+    st = torch.cuda.current_stream()
+    for _ in range(warmup):
+        comm.alltoallv(send, sc, sd, recv, rc, rd, st)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(iters):
+        comm.alltoallv(send, sc, sd, recv, rc, rd, st)
+    e1.record(st)
+    torch.cuda.synchronize()
+    t = max_over(e0.elapsed_time(e1) * 1e-3 / iters)
+    comm.check_async()
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for s in range(R):
+        C.check_payload(recv[rd[s]:], 0, rc[s], 9, s, rank, bad)
+    torch.cuda.synchronize()
+    mism = int(max_over(float(bad.item())))
+    tn = None
+    if nccl:
+        out = torch.empty_like(recv)
+        sv, rv = send[:sum(sc)], out[:sum(rc)]
+        for _ in range(warmup):
+            dist.all_to_all_single(rv, sv, list(rc), list(sc), group=pg)
+        torch.cuda.synchronize()
+        dist.barrier()
+        n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n0.record()
+        for _ in range(iters):
+            dist.all_to_all_single(rv, sv, list(rc), list(sc), group=pg)
+        n1.record()
+        torch.cuda.synchronize()
+        tn = max_over(n0.elapsed_time(n1) * 1e-3 / iters)
+    comm.deregister(hs)
+    comm.deregister(hr)
+    total = sum(m)
+    bound = port_bound(m, R)
+    relays = 0
+    if fabric == "alltoall":
+        t_ = P.build_canonical(1, R, 0, 900e9, 0, P.ALLTOALL)
+        relays = sum(1 for pp in P.plan(t_, R, R, m).pairs for c, _ in pp.flows if c > 0)
+    row = {"case": name, "ranks": R, "fabric_model": fabric, "total_bytes": total, "us": t * 1e6,
+           "gbps": total / t / 1e9, "bound_us": bound * 1e6, "frac_of_bound": bound / t if t else None,
+           "nccl_us": tn * 1e6 if tn else None, "nccl_gbps": total / tn / 1e9 if tn else None,
+           "vs_nccl": (tn / t) if tn else None, "relay_flows": relays, "mismatched_bytes": mism}
+    if extra:
+        row.update(extra)
+    if rank == 0:
+        print(json.dumps(row), flush=True)
+    return row
+
+
+def main():
+    os.environ["NCCL_DEBUG"] = "WARN"
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+    dist.init_process_group("gloo")
+    pg = dist.new_group(backend="nccl")
+    uid = [C.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, 0)
+    comm = C.Comm.init_rank(world, uid[0], rank)
+    if os.environ.get("SWEEP_PULL"):
+        comm.set_config(pull=int(os.environ["SWEEP_PULL"]))
+    R = world
+    cases = os.environ.get("SWEEP_CASES", "c3,c5,c4,c1,c2").split(",")
+    if "c3" in cases:
+        for i in range(10):
+            run_point(comm, pg, rank, R, P.gen_skewed_a2av(R, 256 * MiB, i / 10, 0), "c3", extra={"ratio": i / 10})
+    if "c5" in cases:
+        run_point(comm, pg, rank, R, P.gen_skewed_a2av(R, 256 * MiB, 1.0 / (R - 1), 0), "c5")
+    if "c4" in cases:
+        t = 1024
+        while t <= 1 << 30:
+            run_point(comm, pg, rank, R, P.gen_irregular(R, t, 0.5, 1), "c4", extra={"total": t})
+            t *= 16
+    if "c1" in cases and R == 3:
+        for fab in ("nvswitch", "alltoall"):
+            run_point(comm, pg, rank, R, P.gen_p2p(R, 0, 1, 64 * MiB), "c1", fab)
+    if "c2" in cases and R == 4:
+        for fab in ("nvswitch", "alltoall"):
+            run_point(comm, pg, rank, R, P.gen_p2p(R, 0, 1, 1 << 30), "c2", fab, iters=5)
+    dist.barrier()
+    comm.destroy()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
