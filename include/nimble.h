@@ -179,8 +179,10 @@ typedef struct {
     int gpus_per_node;            /* model GPUs (>= nranks); idle ones relay */
     double nvlink_bytes_per_s;    /* per link / port                          */
     nimblePlannerConfig planner;
-    uint64_t pipe_chunk;          /* relay staging slot size, 512 KiB (pipeline.hpp:19) */
-    uint64_t p2p_buffer;          /* staging bytes per ring, 10 MiB (pipeline.hpp:18)   */
+    uint64_t pipe_chunk;          /* relay staging slot size, 64 KiB (reference: 512 KiB,
+                                     pipeline.hpp:19; finer slots keep more CTAs busy)  */
+    uint64_t p2p_buffer;          /* staging bytes per ring, 10 MiB (pipeline.hpp:18);
+                                     slots = channels * p2p_buffer / pipe_chunk <= 256  */
     int channels_per_peer;        /* rings per relayed flow, 1 (pipeline.hpp:23)        */
     int ctas;                     /* forwarding-engine CTAs per launch, 0 = auto        */
     uint64_t direct_chunk;        /* work-item size of direct pushes/pulls, self rings and

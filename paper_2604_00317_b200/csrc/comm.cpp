@@ -270,7 +270,7 @@ uint32_t slot_count(const nimbleCommConfig& cfg) {
     if (cfg.pipe_chunk == 0) throw Error(nimbleInvalidArgument, "config: pipe_chunk must be positive");
     const uint64_t s = static_cast<uint64_t>(cfg.channels_per_peer) * (cfg.p2p_buffer / cfg.pipe_chunk);
     if (s == 0) throw Error(nimbleInvalidArgument, "config: p2p_buffer holds less than one chunk");
-    if (s > kMaxSlots) throw Error(nimbleInvalidArgument, "config: more than 64 staging slots per ring");
+    if (s > kMaxSlots) throw Error(nimbleInvalidArgument, "config: more than 256 staging slots per ring");
     return static_cast<uint32_t>(s);
 }
 
@@ -284,7 +284,10 @@ void default_config(nimbleCommConfig* cfg, int nranks) {
     cfg->gpus_per_node = nranks;
     cfg->nvlink_bytes_per_s = 900e9;
     nimblePlannerConfigDefault(&cfg->planner);
-    cfg->pipe_chunk = 512ull << 10;
+    // Same 10 MiB per ring as the reference's PipelineConfig (pipeline.hpp:18),
+    // cut finer: 160 x 64 KiB slots keep ~160 CTAs busy on one relayed flow
+    // (20 x 512 KiB capped it at 20).
+    cfg->pipe_chunk = 64ull << 10;
     cfg->p2p_buffer = 10ull << 20;
     cfg->channels_per_peer = 1;
     cfg->ctas = 0;
@@ -572,7 +575,8 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
         a.trace = c->d_trace;
     }
     int ctas = c->cfg.ctas > 0 ? c->cfg.ctas : c->sms;
-    ctas = std::max(1, std::min(ctas, c->sms));
+    // small exchanges: no more CTAs than items (each CTA costs a fence at exit)
+    ctas = std::max(1, std::min({ctas, c->sms, static_cast<int>(std::max<size_t>(cs.sc.items.size(), 1))}));
     // every rank launches even with nothing to move: its posts and done
     // flags are what its peers wait for
     CUDA_TRY(launch_exchange(a, ctas, st));

@@ -25,7 +25,7 @@
 namespace nb {
 
 constexpr int kMaxRanks = 32;
-constexpr int kMaxSlots = 64;
+constexpr int kMaxSlots = 256;
 constexpr int kThreads = 512;  // forwarding-engine CTA size
 
 enum ItemKind : uint8_t {

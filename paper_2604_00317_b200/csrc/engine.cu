@@ -50,8 +50,10 @@ constexpr int kStageBytes = 32 * 1024;          // bytes of output per stage
 constexpr int kStageVecs = kStageBytes / 16;
 constexpr int kStages = 6;                      // ring depth
 constexpr int kStagePitch = kStageBytes + 128;  // + realignment overhang, 128 B aligned
-constexpr int kConsumerWarps = kThreads / 32 - 1;
+constexpr int kConsumerWarps = kThreads / 32 - 2;  // warp 0 produces, the last warp signals
 constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kSignalWarp = kThreads / 32 - 1;
+constexpr int kSig = 32;                            // in-flight item-end signals per CTA
 
 __device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
     uint64_t v;
@@ -171,6 +173,18 @@ struct StageDesc {
     uint32_t action;
     uint64_t head_src, head_dst, tail_src, tail_dst;
     uint32_t head_n, tail_n;
+    uint32_t sig;  // signal-ring entry of the item's end actions
+    // filled by prepare() for the producer's use only (copied into the SigDesc)
+    uint64_t* flag1;
+    uint64_t tag1;
+    uint64_t* flag2;
+    uint64_t tag2;
+};
+
+// Item-end actions handed from the consumers to the signal warp, which does
+// the system fence and the flag releases off the data path.
+struct SigDesc {
+    uint32_t action, terminate;
     uint64_t* flag1;
     uint64_t tag1;
     uint64_t* flag2;
@@ -181,6 +195,9 @@ struct SharedState {
     uint64_t full[kStages];
     uint64_t empty[kStages];
     StageDesc desc[kStages];
+    uint64_t sig_full[kSig];   // consumers (one arrive per warp) -> signal warp
+    uint64_t sig_empty[kSig];  // signal warp -> producer
+    SigDesc sig[kSig];
     uint64_t seg_base[kMaxRanks * kMaxRanks];  // (receiver, sender) -> resolved segment base
     uint32_t seg_mode[kMaxRanks * kMaxRanks];  // 0 = unresolved
     uint64_t send_base[kMaxRanks];             // sender -> its registered send segment (pull)
@@ -321,7 +338,13 @@ __device__ __forceinline__ void trace_max(const LaunchArgs& a, int slot) {
 
 __device__ void produce(SharedState& sh, uint8_t* stages, const LaunchArgs& a) {
     uint32_t* scratch = a.comm->scratch;
-    uint32_t cnt = 0;
+    uint32_t cnt = 0, nsig = 0;
+    auto next_sig = [&]() {
+        const uint32_t j = nsig % kSig;
+        if (nsig >= kSig) mbar_wait(&sh.sig_empty[j], ((nsig / kSig) - 1) & 1);
+        ++nsig;
+        return j;
+    };
     bool first = true;
     auto next_slot = [&](uint32_t& slot) {
         slot = cnt % kStages;
@@ -338,6 +361,17 @@ __device__ void produce(SharedState& sh, uint8_t* stages, const LaunchArgs& a) {
         if (first) {
             trace_min(a, kTraceFirstItem);
             first = false;
+        }
+        uint32_t sig = 0;
+        if (end.action) {
+            sig = next_sig();
+            SigDesc& sd = sh.sig[sig];
+            sd.action = end.action;
+            sd.terminate = 0;
+            sd.flag1 = end.flag1;
+            sd.tag1 = end.tag1;
+            sd.flag2 = end.flag2;
+            sd.tag2 = end.tag2;
         }
         // head: bytes until the destination is 16-byte aligned
         uint64_t n = it.bytes;
@@ -370,10 +404,7 @@ __device__ void produce(SharedState& sh, uint8_t* stages, const LaunchArgs& a) {
                 ds.tail_src = bsrc + (n16 << 4);
                 ds.tail_dst = bdst + (n16 << 4);
                 ds.tail_n = tail;
-                ds.flag1 = end.flag1;
-                ds.tag1 = end.tag1;
-                ds.flag2 = end.flag2;
-                ds.tag2 = end.tag2;
+                ds.sig = sig;
             }
             uint32_t bytes = 0;
             if (nvec) {
@@ -396,6 +427,26 @@ __device__ void produce(SharedState& sh, uint8_t* stages, const LaunchArgs& a) {
     next_slot(slot);
     sh.desc[slot].flags = kTerminate;
     mbar_arrive(&sh.full[slot]);
+    const uint32_t j = next_sig();  // and stop the signal warp
+    sh.sig[j].terminate = 1;
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&sh.sig_full[j])),
+                 "r"(kConsumerWarps)
+                 : "memory");
+}
+
+// Signal warp (lane 0): item-end flag releases, in item order, one fence per
+// batch of completed items.
+__device__ void signal_loop(SharedState& sh) {
+    for (uint32_t n = 0;; ++n) {
+        const uint32_t j = n % kSig;
+        mbar_wait(&sh.sig_full[j], (n / kSig) & 1);
+        const SigDesc sd = sh.sig[j];
+        if (sd.terminate) break;
+        asm volatile("fence.acq_rel.sys;" ::: "memory");  // the item's bytes before its flag
+        if (sd.action & kActRelease1) st_relaxed(sd.flag1, sd.tag1);
+        if (sd.action & kActRelease2) st_relaxed(sd.flag2, sd.tag2);
+        mbar_arrive(&sh.sig_empty[j]);
+    }
 }
 
 template <int q>
@@ -442,11 +493,9 @@ __device__ void consume(SharedState& sh, const uint8_t* stages, const LaunchArgs
             if (ct >= 32 && ct < 32 + static_cast<int>(ds.tail_n))
                 reinterpret_cast<uint8_t*>(ds.tail_dst)[ct - 32] =
                     ld_byte(reinterpret_cast<const uint8_t*>(ds.tail_src) + (ct - 32), coh);
-            if (ds.action) asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
-            if (ct == 0 && ds.action) {
-                __threadfence_system();
-                if (ds.action & kActRelease1) st_release(ds.flag1, ds.tag1);
-                if (ds.action & kActRelease2) st_release(ds.flag2, ds.tag2);
+            if (ds.action) {  // hand the item to the signal warp (no fence on the data path)
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sh.sig_full[ds.sig]);
             }
         }
     }
@@ -474,6 +523,10 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
             mbar_init(&sh.full[s], 1);
             mbar_init(&sh.empty[s], kConsumerWarps);
         }
+        for (int j = 0; j < kSig; ++j) {
+            mbar_init(&sh.sig_full[j], kConsumerWarps);
+            mbar_init(&sh.sig_empty[j], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // Prologue: publish where each sender's segment lands in my buffer.
@@ -494,8 +547,11 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
     __syncthreads();
     if (tid == 0 && blockIdx.x == 0) trace_max(a, kTracePrologueDone);
 
-    if (tid < 32) {
+    const int warp = tid / 32;
+    if (warp == 0) {
         if (tid == 0) produce(sh, stages, a);
+    } else if (warp == kSignalWarp) {
+        if ((tid & 31) == 0) signal_loop(sh);
     } else {
         consume(sh, stages, a);
     }
