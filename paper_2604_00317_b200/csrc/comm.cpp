@@ -461,6 +461,9 @@ int window_of(const nimbleComm* c, uint64_t ptr, uint64_t n) {
 // self ring (staged); where each outgoing segment lives (registered windows
 // can be pulled by their receiver); whether this rank asks to pull.
 void fill_posts(nimbleComm* c, RankBuffers& rb) {
+    for (int p = 0; p < rb.R; ++p)
+        if (rb.send_bytes[p] >> 48 || rb.recv_bytes[p] >> 48 || rb.recv_ptr[p] >> 48)
+            throw Error(nimbleInvalidArgument, "alltoallv: segments must be < 2^48 bytes and addresses < 2^48");
     uint64_t ingress = 0, egress = 0;
     for (int p = 0; p < rb.R; ++p)
         if (p != rb.me) ingress += rb.recv_bytes[p], egress += rb.send_bytes[p];

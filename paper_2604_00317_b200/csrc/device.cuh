@@ -70,11 +70,22 @@ struct Post {
 };
 static_assert(sizeof(Post) == 32, "Post layout");
 
+// A post as published in ctrl: low-latency encoding with the epoch inside
+// every 8-byte word, so it is written with plain relaxed stores (no fence) and
+// a reader accepts it once all three words carry its epoch:
+//   w[0] = epoch32 << 32 | win << 16 | mode,  w[1] = epoch16 << 48 | off,
+//   w[2] = epoch16 << 48 | bytes            (off, bytes < 2^48).
+// Double-buffered by epoch parity: epoch e's post stays intact until every
+// peer has finished epoch e (no rank can reach e + 2 before that).
+struct WirePost {
+    uint64_t w[4];
+};
+
 struct CtrlHeader {
-    Post post[kMaxRanks];       // written by me (the receiver), read by writers
-    uint64_t done[kMaxRanks];   // done[w] = epoch: writer w finished writing into me
-    Post send_post[kMaxRanks];  // written by me (the sender), read by pulling receivers
-    uint64_t pulled[kMaxRanks]; // pulled[d] = epoch: receiver d finished pulling from me
+    WirePost post[2][kMaxRanks];       // written by me (the receiver), read by writers
+    uint64_t done[kMaxRanks];          // done[w] = epoch: writer w finished writing into me
+    WirePost send_post[2][kMaxRanks];  // written by me (the sender), read by pulling receivers
+    uint64_t pulled[kMaxRanks];        // pulled[d] = epoch: receiver d finished pulling from me
 };
 
 // Geometry of the flag arrays that follow the header inside ctrl.
@@ -101,8 +112,8 @@ struct CommDevice {
     uint32_t nwin;
     uint32_t timeout_ms;
     uint32_t* status;             // host-mapped: [0] error code, [1] detail
-    uint32_t* scratch;            // [0] queue head, [1] CTAs done, [2, 2+kMaxRanks) write counters,
-                                  // [2+kMaxRanks, 2+2*kMaxRanks) pull counters
+    uint32_t* scratch;            // [0] queue head, [1] CTAs done, [2, 2+kMaxRanks) grant decisions
+                                  // as sender, [2+kMaxRanks, 2+2*kMaxRanks) as receiver (kDecide*)
 };
 
 // Per-launch arguments (passed by value as a __grid_constant__ kernel parameter).

@@ -202,20 +202,70 @@ struct SharedState {
     uint32_t seg_mode[kMaxRanks * kMaxRanks];  // 0 = unresolved
     uint64_t send_base[kMaxRanks];             // sender -> its registered send segment (pull)
     uint32_t send_mode[kMaxRanks];             // 0 = unresolved
+    uint32_t remote_writes;                    // this CTA stored into peer memory
 };
+
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+struct PostView {
+    uint32_t mode, win;
+    uint64_t off, bytes;
+};
+
+// Wait for this epoch's post at p and decode it.  False (async error) on timeout.
+__device__ bool read_post(const WirePost* p, uint64_t epoch, const CommDevice* c, PostView& out) {
+    const uint64_t e32 = epoch & 0xffffffffull, e16 = epoch & 0xffffull;
+    const uint64_t t0 = global_ns();
+    const uint64_t limit = static_cast<uint64_t>(c->timeout_ms) * 1000000ull;
+    for (uint32_t spin = 0;; ++spin) {
+        const uint64_t w0 = ld_acquire(&p->w[0]);
+        if ((w0 >> 32) == e32) {
+            const uint64_t w1 = ld_relaxed(&p->w[1]), w2 = ld_relaxed(&p->w[2]);
+            if ((w1 >> 48) == e16 && (w2 >> 48) == e16) {
+                out.mode = static_cast<uint32_t>(w0 & 0xffff);
+                out.win = static_cast<uint32_t>((w0 >> 16) & 0xffff);
+                out.off = w1 & 0xffffffffffffull;
+                out.bytes = w2 & 0xffffffffffffull;
+                return true;
+            }
+        }
+        if ((spin & 255) == 255) {
+            if (*reinterpret_cast<volatile uint32_t*>(c->status) != 0) return false;
+            if (global_ns() - t0 > limit) {
+                atomicCAS(c->status, 0u, static_cast<uint32_t>(kErrPostTimeout));
+                return false;
+            }
+        }
+        if (spin > 64) __nanosleep(32);
+    }
+}
+
+__device__ __forceinline__ void write_post(WirePost* p, uint64_t epoch, const Post& v) {
+    const uint64_t e16 = (epoch & 0xffffull) << 48;
+    st_relaxed(&p->w[1], e16 | (v.off & 0xffffffffffffull));
+    st_relaxed(&p->w[2], e16 | (v.bytes & 0xffffffffffffull));
+    st_relaxed(&p->w[0], (epoch & 0xffffffffull) << 32 | (static_cast<uint64_t>(v.win & 0xffff) << 16) |
+                             (v.mode & 0xffff));
+}
+
+enum Decide : uint32_t { kDecidePull = 1, kDecidePush = 2 };  // per-launch grant records (scratch)
 
 // Resolve receiver d's post for sender s (producer thread).
 __device__ bool resolve(SharedState& sh, const LaunchArgs& a, int d, int s) {
     const int key = d * kMaxRanks + s;
     if (sh.seg_mode[key]) return true;
     const CommDevice* c = a.comm;
-    const Post* p = reinterpret_cast<const Post*>(c->ctrl[d]) + s;
-    if (!wait_ge(&p->tag, a.epoch, c, kErrPostTimeout)) return false;
-    const uint32_t mode = *reinterpret_cast<const volatile uint32_t*>(&p->mode);
-    const uint32_t win = *reinterpret_cast<const volatile uint32_t*>(&p->win);
-    const uint64_t off = *reinterpret_cast<const volatile uint64_t*>(&p->off);
+    PostView v;
+    if (!read_post(&reinterpret_cast<const CtrlHeader*>(c->ctrl[d])->post[a.epoch & 1][s], a.epoch, c, v))
+        return false;
+    const uint32_t mode = v.mode, win = v.win;
+    const uint64_t off = v.off;
     if (s == c->rank) {  // my own outgoing segment: sizes must agree end to end
-        const uint64_t expect = *reinterpret_cast<const volatile uint64_t*>(&p->bytes);
+        const uint64_t expect = v.bytes;
         if (expect != a.send_bytes[d]) {
             atomicCAS(c->status, 0u, static_cast<uint32_t>(kErrSizeMismatch));
             return false;
@@ -223,6 +273,9 @@ __device__ bool resolve(SharedState& sh, const LaunchArgs& a, int d, int s) {
     }
     sh.seg_base[key] = (mode & 0xf) == kPostZeroCopy ? c->win_table[win * kMaxRanks + d] + off : 0;
     sh.seg_mode[key] = mode;
+    if (s == c->rank)  // record, for the epilogue, whether d pulls my segment or takes pushes
+        c->scratch[2 + d] = ((mode & kPostPullRequest) && a.send_posts[d].mode == kSendRegistered) ? kDecidePull
+                                                                                                    : kDecidePush;
     return true;
 }
 
@@ -230,11 +283,12 @@ __device__ bool resolve(SharedState& sh, const LaunchArgs& a, int d, int s) {
 __device__ bool resolve_send(SharedState& sh, const LaunchArgs& a, int s) {
     if (sh.send_mode[s]) return true;
     const CommDevice* c = a.comm;
-    const Post* p = reinterpret_cast<const CtrlHeader*>(c->ctrl[s])->send_post + c->rank;
-    if (!wait_ge(&p->tag, a.epoch, c, kErrPostTimeout)) return false;
-    const uint32_t mode = *reinterpret_cast<const volatile uint32_t*>(&p->mode);
-    const uint32_t win = *reinterpret_cast<const volatile uint32_t*>(&p->win);
-    const uint64_t off = *reinterpret_cast<const volatile uint64_t*>(&p->off);
+    PostView v;
+    if (!read_post(&reinterpret_cast<const CtrlHeader*>(c->ctrl[s])->send_post[a.epoch & 1][c->rank], a.epoch, c, v))
+        return false;
+    const uint32_t mode = v.mode, win = v.win;
+    const uint64_t off = v.off;
+    c->scratch[2 + kMaxRanks + s] = mode == kSendRegistered ? kDecidePull : kDecidePush;
     sh.send_base[s] = mode == kSendRegistered ? c->win_table[win * kMaxRanks + s] + off : 0;
     sh.send_mode[s] = mode;
     asm volatile("fence.proxy.async.global;" ::: "memory");  // generic -> async proxy (TMA reads)
@@ -358,6 +412,8 @@ __device__ void produce(SharedState& sh, uint8_t* stages, const LaunchArgs& a) {
         StageDesc end{};
         bool coherent = false;
         if (prepare(sh, a, it, src, dst, end, coherent) != kGo) continue;
+        if (it.kind == kPush || it.kind == kStage || (it.kind == kForward && it.peer != a.comm->rank))
+            sh.remote_writes = 1;
         if (first) {
             trace_min(a, kTraceFirstItem);
             first = false;
@@ -518,6 +574,7 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
     if (tid == 0) trace_min(a, kTraceKernelStart);
     for (int i = tid; i < kMaxRanks * kMaxRanks; i += kThreads) sh.seg_mode[i] = 0;
     for (int i = tid; i < kMaxRanks; i += kThreads) sh.send_mode[i] = 0;
+    if (tid == 0) sh.remote_writes = 0;
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&sh.full[s], 1);
@@ -536,12 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
         const Post p = send_side ? a.send_posts[peer] : a.posts[peer];
         if (p.tag) {
             CtrlHeader* h = reinterpret_cast<CtrlHeader*>(c->ctrl[me]);
-            Post* mine = (send_side ? h->send_post : h->post) + peer;
-            mine->win = p.win;
-            mine->mode = p.mode;
-            mine->off = p.off;
-            mine->bytes = p.bytes;
-            st_release(&mine->tag, a.epoch);
+            write_post((send_side ? h->send_post : h->post)[a.epoch & 1] + peer, a.epoch, p);
         }
     }
     __syncthreads();
@@ -563,7 +615,10 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
     // for the next stream-ordered launch.
     __shared__ uint32_t last_cta;
     if (tid == 0) {
-        __threadfence_system();  // this CTA's peer writes, before the rank-wide completion count
+        // this CTA's peer writes before the rank-wide completion count (pulls
+        // and local copies only read remote memory: a GPU-scope fence will do)
+        if (sh.remote_writes) __threadfence_system();
+        else __threadfence();
         last_cta = atomicAdd(&scratch[1], 1u) + 1 == gridDim.x;
     }
     __syncthreads();
@@ -585,28 +640,18 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
             if (lane < R) {
                 const int w = lane;
                 const CtrlHeader* h = reinterpret_cast<const CtrlHeader*>(c->ctrl[me]);
+                const uint32_t* decide = scratch + 2;
                 bool need_done = (a.relay_writers >> w) & 1;
-                if (((a.recv_direct >> w) & 1) && ((a.recv_zc >> w) & 1)) {  // w pushed in place unless I pulled
-                    bool pulled = false;
-                    if ((a.pull_req >> w) & 1) {
-                        const Post* sp = reinterpret_cast<const CtrlHeader*>(c->ctrl[w])->send_post + me;
-                        if (wait_ge(&sp->tag, a.epoch, c, kErrPostTimeout))
-                            pulled = *reinterpret_cast<const volatile uint32_t*>(&sp->mode) == kSendRegistered;
-                    }
-                    need_done |= !pulled;
-                }
+                if (((a.recv_direct >> w) & 1) && ((a.recv_zc >> w) & 1))  // w pushed in place unless I pulled
+                    need_done |= !(((a.pull_req >> w) & 1) && decide[kMaxRanks + w] == kDecidePull);
                 if (need_done) wait_ge(&h->done[w], a.epoch, c, kErrDoneTimeout);
-                if ((a.push_targets >> w) & 1) {  // receiver w pulled my segment: wait until it has
-                    const Post* rp = reinterpret_cast<const CtrlHeader*>(c->ctrl[w])->post + me;
-                    if (wait_ge(&rp->tag, a.epoch, c, kErrPostTimeout)) {
-                        const uint32_t mode = *reinterpret_cast<const volatile uint32_t*>(&rp->mode);
-                        if ((mode & kPostPullRequest) && a.send_posts[w].mode == kSendRegistered)
-                            wait_ge(&h->pulled[w], a.epoch, c, kErrDoneTimeout);
-                    }
-                }
+                if (((a.push_targets >> w) & 1) && decide[w] == kDecidePull)  // w pulled my segment
+                    wait_ge(&h->pulled[w], a.epoch, c, kErrDoneTimeout);
             }
             __syncwarp();
         }
+        if (lane < R) scratch[2 + lane] = scratch[2 + kMaxRanks + lane] = 0;
+        __syncwarp();
         if (lane == 0) {
             trace_max(a, kTraceWaited);
             scratch[0] = 0;
