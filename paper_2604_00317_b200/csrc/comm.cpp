@@ -460,7 +460,7 @@ int window_of(const nimbleComm* c, uint64_t ptr, uint64_t n) {
 // Where each incoming segment lands: a registered window (zero copy) or the
 // self ring (staged); where each outgoing segment lives (registered windows
 // can be pulled by their receiver); whether this rank asks to pull.
-void fill_posts(nimbleComm* c, RankBuffers& rb) {
+void fill_posts(nimbleComm* c, RankBuffers& rb, const PlanResult& plan) {
     for (int p = 0; p < rb.R; ++p)
         if (rb.send_bytes[p] >> 48 || rb.recv_bytes[p] >> 48 || rb.recv_ptr[p] >> 48)
             throw Error(nimbleInvalidArgument, "alltoallv: segments must be < 2^48 bytes and addresses < 2^48");
@@ -485,6 +485,12 @@ void fill_posts(nimbleComm* c, RankBuffers& rb) {
         }
         rb.send_post[static_cast<size_t>(d)] = p;
     }
+    // a pair whose plan relays part of it takes pushes only: its relays push
+    // into my port anyway, and pulling beside them was measured slower
+    std::vector<char> relayed(static_cast<size_t>(rb.R), 0);
+    for (const PairRoutes& pr : plan.pairs)
+        if (pr.dst == rb.me)
+            for (const Flow& f : pr.flows) relayed[static_cast<size_t>(pr.src)] |= pr.cands[static_cast<size_t>(f.cand)].via >= 0;
     rb.recv_post.assign(static_cast<size_t>(rb.R), Post{});
     for (int s = 0; s < rb.R; ++s) {
         if (s == rb.me || rb.recv_bytes[s] == 0) continue;
@@ -499,7 +505,7 @@ void fill_posts(nimbleComm* c, RankBuffers& rb) {
             p.win = static_cast<uint32_t>(w);
             p.off = rb.recv_ptr[s] - c->windows[static_cast<size_t>(w)].base;
         }
-        if (rb.pull) p.mode |= kPostPullRequest;
+        if (rb.pull && !relayed[static_cast<size_t>(s)]) p.mode |= kPostPullRequest;
         rb.recv_post[static_cast<size_t>(s)] = p;
     }
 }
@@ -626,7 +632,7 @@ void run_exchanges(std::vector<Exchange>& exs) {
         for (int p = 0; p < R; ++p) m[static_cast<size_t>(p) * R + p] = 0;
         uint64_t plan_id = 0;
         std::shared_ptr<PlanResult> plan = plan_for(c, m, &plan_id);
-        fill_posts(c, ex.rb);
+        fill_posts(c, ex.rb, *plan);
         CachedSchedule& cs = schedule_for(c, plan_id, *plan, ex.rb, ex.stream);
         std::vector<cudaEvent_t> evs;
         for (cudaStream_t o : ex.others) {

@@ -104,7 +104,7 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
                 }
                 if (d == me) {
                     sc.recv_direct |= 1ull << s;
-                    if (rb.pull) {  // receiver-driven: used if the sender grants it at run time
+                    if (rb.recv_post[s].mode & kPostPullRequest) {  // used if the sender grants it at run time
                         sc.pull_req |= 1ull << s;
                         Item proto{};
                         proto.kind = kPull;

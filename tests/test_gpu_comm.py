@@ -135,6 +135,47 @@ def w_repeat_mixed(comm, rank, R):
     return res
 
 
+def w_stress_back_to_back(comm, rank, R):
+    """Many exchanges queued back to back without host syncs: alternating
+    matrices, buffers, registrations and push/pull modes (epoch-parity posts,
+    flag tags, schedule cache), each verified afterwards."""
+    import random
+    from paper_2604_00317_b200 import comm as C
+    from paper_2604_00317_b200 import planner as P
+    rng = random.Random(7)  # same sequence on every rank
+    pool = []
+    for it in range(3):
+        m = P.gen_skewed_a2av(R, (1 + 3 * it) * MiB + 11 * it, 0.2 + 0.3 * it, it % R)
+        sc, sd, rc, rd = C.packed_displs(m, R, rank)
+        send = torch.empty(max(sum(sc), 16), dtype=torch.uint8, device="cuda")
+        for d in range(R):
+            C.fill_payload(send[sd[d]:], 0, sc[d], 50 + it, rank, d)
+        recvs = [torch.zeros(max(sum(rc), 16), dtype=torch.uint8, device="cuda") for _ in range(2)]
+        hs = comm.register(send) if it != 1 else None
+        hr = comm.register(recvs[0])
+        pool.append((m, sc, sd, rc, rd, send, recvs, hs, hr, 50 + it))
+    plan = [(rng.randrange(3), rng.randrange(2), rng.choice([1, 2])) for _ in range(40)]
+    for k, (i, j, pull) in enumerate(plan):
+        if k % 10 == 0:
+            comm.set_config(pull=pull)  # a config change is a (host-synchronizing) collective
+        m, sc, sd, rc, rd, send, recvs, hs, hr, seed = pool[i]
+        comm.alltoallv(send, sc, sd, recvs[j], rc, rd)
+    torch.cuda.synchronize()
+    comm.check_async()
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for (m, sc, sd, rc, rd, send, recvs, hs, hr, seed) in pool:
+        for j in range(2):
+            if any(pi == pool.index((m, sc, sd, rc, rd, send, recvs, hs, hr, seed)) and pj == j for pi, pj, _ in plan):
+                for s in range(R):
+                    C.check_payload(recvs[j][rd[s]:], 0, rc[s], seed, s, rank, bad)
+    torch.cuda.synchronize()
+    for (m, sc, sd, rc, rd, send, recvs, hs, hr, seed) in pool:
+        if hs is not None:
+            comm.deregister(hs)
+        comm.deregister(hr)
+    return int(bad.item())
+
+
 def w_sendrecv_ring(comm, rank, R):
     from paper_2604_00317_b200 import comm as C
     n = 5 * MiB + 17
@@ -218,6 +259,12 @@ def test_repeated_mixed_exchanges():
     R = min(_ngpus(), 4)
     for r, res in _spawn("w_repeat_mixed", R).items():
         assert all(bad == 0 and ok for bad, ok in res), (r, res)
+
+
+@need2
+def test_stress_back_to_back_exchanges():
+    R = min(_ngpus(), 4)
+    assert all(v == 0 for v in _spawn("w_stress_back_to_back", R).values())
 
 
 @need2

@@ -22,10 +22,13 @@ def main():
     dist.broadcast_object_list(uid, 0)
     comm = C.Comm.init_rank(world, uid[0], rank)
     R = world
+    case = os.environ.get("TRACE_CASE", "skew")
+    if case == "relay":
+        comm.set_config(fabric="alltoall", gpus_per_node=R)
     for pull in (1, 2):
         comm.set_config(pull=pull)
-        for mib in (1, 256):
-            m = P.gen_skewed_a2av(R, mib * MiB, 0.7, 0)
+        for mib in ((64, 1024) if case == "relay" else (1, 256)):
+            m = P.gen_p2p(R, 0, 1, mib * MiB) if case == "relay" else P.gen_skewed_a2av(R, mib * MiB, 0.7, 0)
             sc, sd, rc, rd = C.packed_displs(m, R, rank)
             send = torch.empty(max(sum(sc), 16), dtype=torch.uint8, device="cuda")
             recv = torch.empty(max(sum(rc), 16), dtype=torch.uint8, device="cuda")
