@@ -276,6 +276,26 @@ nimbleResult_t nimbleBenchMatrix(nimbleComm_t comm, const uint64_t* matrix, int 
 nimbleResult_t nimbleBootstrapAllgather(const nimbleUniqueId* id, int rank, int nranks, const void* in, size_t n,
                                         void* out);
 
+/* The chunk scheduler, host only: the ordered work items rank `rank` would
+ * run for `plan` (from nimblePlanCreate / nimblePlanDirect over `ranks` ranks,
+ * packed layout).  recv_staged_mask bit s: my receive segment from s is not
+ * registered (drained through my self ring); pull_mask bit s: I ask s to let
+ * me pull.  Items are written as nimbleItem records in execution order;
+ * addresses are synthetic: send segment for d at (1 + rank) << 40 + sdispl[d],
+ * receive segment from s at (17 + rank) << 40 + rdispl[s]. */
+typedef struct {
+    uint64_t src, dst;  /* absolute (local kinds) or offset inside the pair segment */
+    uint32_t bytes;
+    uint8_t kind;       /* 0 local, 1 push, 2 stage, 3 forward, 4 pull */
+    uint8_t peer;       /* receiver (push/forward), relay (stage), sender (pull) */
+    uint16_t aux;       /* final receiver (stage), original sender (forward) */
+    uint32_t seq;       /* chunk index inside its ring / flow */
+    uint32_t pad;
+} nimbleItem;
+nimbleResult_t nimbleDebugSchedule(nimblePlan_t plan, int rank, int ranks, uint64_t pipe_chunk, uint32_t slots,
+                                   uint64_t direct_chunk, uint64_t recv_staged_mask, uint64_t pull_mask,
+                                   nimbleItem* items, int cap, int* nitems);
+
 /* Device timeline of the comm's last launch (%globaltimer ns): kernel start,
  * prologue done, first item, last item, CTAs done, completions signalled,
  * completions observed.  Needs NIMBLE_TRACE=1 at comm creation; n >= 8. */

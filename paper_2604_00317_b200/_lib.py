@@ -45,6 +45,12 @@ class UniqueId(ctypes.Structure):  # nimbleUniqueId
     _fields_ = [("internal", ctypes.c_char * 128)]
 
 
+class Item(ctypes.Structure):  # nimbleItem (mirrors the engine's 32-byte work item)
+    _fields_ = [("src", c_u64), ("dst", c_u64), ("bytes", ctypes.c_uint32), ("kind", ctypes.c_uint8),
+                ("peer", ctypes.c_uint8), ("aux", ctypes.c_uint16), ("seq", ctypes.c_uint32),
+                ("pad", ctypes.c_uint32)]
+
+
 class BenchResult(ctypes.Structure):  # nimbleBenchResult
     _fields_ = [("seconds_median", c_double), ("seconds_min", c_double), ("gbps_effective", c_double),
                 ("bound_seconds", c_double), ("plan_seconds", c_double), ("total_bytes", c_u64),
@@ -115,6 +121,8 @@ SIGNATURES = {
     "nimbleBenchMatrix": [c_void_p, P(c_u64), c_int, c_int, P(BenchResult)],
     "nimbleBootstrapAllgather": [P(UniqueId), c_int, c_int, c_void_p, c_size, c_void_p],
     "nimbleCommDebugTrace": [c_void_p, P(c_u64), c_int],
+    "nimbleDebugSchedule": [c_void_p, c_int, c_int, c_u64, ctypes.c_uint32, c_u64, c_u64, c_u64, c_void_p, c_int,
+                            P(c_int)],
 }
 _RESTYPES = {"nimbleGetErrorString": c_char_p, "nimbleGetLastError": c_char_p}
 

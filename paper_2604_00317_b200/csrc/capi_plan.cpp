@@ -1,5 +1,6 @@
 // C ABI, group 1: link-load model, traffic-matrix ingest, planner.
 // Host-only; exceptions from the C++ core become result codes here.
+#include <algorithm>
 #include <cstring>
 #include <new>
 #include <stdexcept>
@@ -10,6 +11,7 @@
 #include "demand.hpp"
 #include "fabric.hpp"
 #include "planner.hpp"
+#include "schedule.hpp"
 
 struct nimbleTopology {
     nb::LinkModel lm;
@@ -335,6 +337,46 @@ nimbleResult_t nimblePlanMaxNormalizedLoad(nimblePlan_t p, double* s) {
 nimbleResult_t nimblePlanToJson(nimblePlan_t p, char* out, size_t cap, size_t* need) {
     if (!p) return fail(nimbleInvalidArgument, "plan: null handle");
     return nb::write_text(nb::plan_json(p->plan), out, cap, need);
+}
+
+nimbleResult_t nimbleDebugSchedule(nimblePlan_t p, int rank, int ranks, uint64_t pipe_chunk, uint32_t slots,
+                                   uint64_t direct_chunk, uint64_t staged, uint64_t pull, nimbleItem* items, int cap,
+                                   int* nitems) {
+    static_assert(sizeof(nimbleItem) == sizeof(nb::Item), "nimbleItem mirrors the engine's Item");
+    return nb::guarded([&] {
+        if (!p || !nitems || ranks < 1 || ranks > nb::kMaxRanks || rank < 0 || rank >= ranks)
+            throw std::invalid_argument("schedule: bad argument");
+        std::vector<uint64_t> m(static_cast<size_t>(ranks) * ranks, 0);
+        for (const nb::PairRoutes& pr : p->plan.pairs) m[static_cast<size_t>(pr.src) * ranks + pr.dst] = pr.demand;
+        nb::RankBuffers rb;
+        rb.R = ranks;
+        rb.me = rank;
+        rb.send_ptr.assign(ranks, 0);
+        rb.send_bytes.assign(ranks, 0);
+        rb.recv_ptr.assign(ranks, 0);
+        rb.recv_bytes.assign(ranks, 0);
+        rb.recv_post.assign(ranks, nb::Post{});
+        rb.send_post.assign(ranks, nb::Post{});
+        uint64_t so = 0, ro = 0;
+        for (int q = 0; q < ranks; ++q) {
+            rb.send_bytes[q] = m[static_cast<size_t>(rank) * ranks + q];
+            rb.send_ptr[q] = (static_cast<uint64_t>(1 + rank) << 40) + so;
+            so += rb.send_bytes[q];
+            rb.recv_bytes[q] = m[static_cast<size_t>(q) * ranks + rank];
+            rb.recv_ptr[q] = (static_cast<uint64_t>(17 + rank) << 40) + ro;
+            ro += rb.recv_bytes[q];
+            if (q != rank && rb.recv_bytes[q]) {
+                nb::Post& post = rb.recv_post[q];
+                post.tag = 1;
+                post.bytes = rb.recv_bytes[q];
+                post.mode = ((staged >> q) & 1) ? nb::kPostStaged : nb::kPostZeroCopy;
+                if ((pull >> q) & 1) post.mode |= nb::kPostPullRequest;
+            }
+        }
+        nb::Schedule sc = nb::build_schedule(p->plan, rb, pipe_chunk, slots, direct_chunk);
+        *nitems = static_cast<int>(sc.items.size());
+        if (items) std::memcpy(items, sc.items.data(), std::min<size_t>(sc.items.size(), cap > 0 ? cap : 0) * sizeof(nb::Item));
+    });
 }
 
 }  // extern "C"

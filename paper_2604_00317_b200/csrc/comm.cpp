@@ -564,9 +564,6 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     a.posts = cs.posts.p;
     a.send_posts = cs.send_posts.p;
     for (int r = 0; r < c->nranks; ++r) {
-        a.push_items[r] = cs.sc.push_items[r];
-        a.fwd_items[r] = cs.sc.fwd_items[r];
-        a.pull_items[r] = cs.sc.pull_items[r];
         a.send_bytes[r] = rb.send_bytes[r];
     }
     a.recv_direct = cs.sc.recv_direct;

@@ -126,9 +126,6 @@ struct LaunchArgs {
     const CommDevice* comm;
     const Post* posts;       // [R] my receive posts for this call (device copy)
     const Post* send_posts;  // [R] my send posts for this call (device copy)
-    uint32_t push_items[kMaxRanks];   // kPush items to receiver d (count toward done if zero copy)
-    uint32_t fwd_items[kMaxRanks];    // kForward items into receiver d != me
-    uint32_t pull_items[kMaxRanks];   // kPull items from sender s
     uint64_t recv_direct;             // senders with a direct flow into me
     uint64_t recv_zc;                 // ... whose segment lands in a registered window of mine
     uint64_t pull_req;                // ... from whom I asked to pull

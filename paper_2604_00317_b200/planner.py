@@ -307,3 +307,30 @@ def port_bound_seconds(matrix, ranks, port_bytes_per_s=900e9):
         worst = max(worst, sum(matrix[v * ranks:(v + 1) * ranks]),
                     sum(matrix[s * ranks + v] for s in range(ranks)))
     return worst / port_bytes_per_s
+
+
+def debug_schedule(topo: Topology, ranks, ranks_per_node, matrix, rank, config: PlannerConfig | None = None,
+                   pipe_chunk=64 * KiB, slots=160, direct_chunk=64 * KiB, staged_mask=0, pull_mask=0):
+    """The chunk scheduler's ordered work items for `rank` (nimbleDebugSchedule).
+
+    Returns a list of dicts (kind, peer, aux, seq, src, dst, bytes).  The plan
+    is mcf_plan on `topo` over the off-diagonal demands (self segments are
+    plain local copies and are not part of it).
+    """
+    off_diag = [0 if i // ranks == i % ranks else v for i, v in enumerate(matrix)]
+    cfg = (config or PlannerConfig()).to_c()
+    h = c_void_p()
+    _lib.call("nimblePlanCreate", topo.handle, ranks, ranks_per_node, _lib.u64_array(off_diag), ctypes.byref(cfg),
+              ctypes.byref(h))
+    try:
+        n = c_int()
+        _lib.call("nimbleDebugSchedule", h, rank, ranks, pipe_chunk, slots, direct_chunk, staged_mask, pull_mask,
+                  None, 0, ctypes.byref(n))
+        items = (_lib.Item * max(n.value, 1))()
+        _lib.call("nimbleDebugSchedule", h, rank, ranks, pipe_chunk, slots, direct_chunk, staged_mask, pull_mask,
+                  items, n.value, ctypes.byref(n))
+    finally:
+        _lib.lib().nimblePlanDestroy(h)
+    kinds = {0: "local", 1: "push", 2: "stage", 3: "forward", 4: "pull"}
+    return [{"kind": kinds[it.kind], "peer": it.peer, "aux": it.aux, "seq": it.seq, "src": it.src, "dst": it.dst,
+             "bytes": it.bytes} for it in items[:n.value]]

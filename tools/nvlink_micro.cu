@@ -203,6 +203,25 @@ static void incast(int n) {
 
 int main(int argc, char** argv) {
     const size_t bytes = 256ull << 20;
+    if (argc > 1 && argv[1][0] == 'o') {  // once per primitive, one way 0 -> 1 (for ncu)
+        Bufs b{};
+        for (int dev = 0; dev < 2; ++dev) {
+            CK(cudaSetDevice(dev));
+            CK(cudaDeviceEnablePeerAccess(dev ^ 1, 0));
+            CK(cudaMalloc(dev ? &b.src1 : &b.src0, bytes));
+            CK(cudaMalloc(dev ? &b.dst1 : &b.dst0, bytes));
+            CK(cudaMemset(dev ? b.src1 : b.src0, 1, bytes));
+            CK(cudaFuncSetAttribute(k_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 49152));
+        }
+        CK(cudaSetDevice(0));
+        k_simt<<<148, 512>>>((const uint4*)b.src0, (uint4*)b.dst1, bytes / 16);              // push STG
+        k_tma<4><<<148, 32, 4 * 32768>>>(b.src0, b.dst1, bytes, 32768);                      // push TMA
+        k_tma<4><<<148, 32, 4 * 32768>>>(b.src1, b.dst0, bytes, 32768);                      // pull TMA
+        k_simt<<<148, 512>>>((const uint4*)b.src1, (uint4*)b.dst0, bytes / 16);              // pull LDG
+        CK(cudaDeviceSynchronize());
+        std::printf("once done\n");
+        return 0;
+    }
     if (argc > 1 && argv[1][0] == 'i') {
         int n = 0;
         CK(cudaGetDeviceCount(&n));
