@@ -141,6 +141,54 @@ class Clocks:
                 "samples": len(sm)}
 
 
+def pipelined_e2e(ksteps, slots, run, max_fn=lambda x: x):
+    """End-to-end steps with host-resident inputs and outputs, pipelined the
+    way a user streams host data: two device buffer slots, H2D on one stream,
+    the exchange on a second, D2H on a third, so step k+1's H2D overlaps step
+    k's D2H (PCIe is full duplex).  Every step moves its inputs host->device
+    and its results device->host inside the timed region.
+
+    slots: [(h2d_pairs, d2h_pairs)] per slot, each pair (dst, src) tensors;
+    run(slot, stream) launches the exchange for that slot."""
+    import torch
+    s_in, s_ex, s_out = (torch.cuda.Stream() for _ in range(3))
+    ev = lambda: torch.cuda.Event()  # noqa: E731
+    h2d_done = [ev() for _ in slots]
+    ex_done = [ev() for _ in slots]
+    d2h_done = [None for _ in slots]
+
+    def step(k):
+        j = k % len(slots)
+        h2d, d2h = slots[j]
+        with torch.cuda.stream(s_in):
+            if d2h_done[j] is not None:
+                s_in.wait_event(d2h_done[j])  # slot j fully drained by step k-2
+            for dst, src in h2d:
+                dst.copy_(src, non_blocking=True)
+            h2d_done[j].record(s_in)
+        s_ex.wait_event(h2d_done[j])
+        run(j, s_ex)
+        ex_done[j].record(s_ex)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(ex_done[j])
+            for dst, src in d2h:
+                dst.copy_(src, non_blocking=True)
+            d2h_done[j] = ev()
+            d2h_done[j].record(s_out)
+
+    for k in range(len(slots)):  # warm both slots
+        step(k)
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s_in)
+    for k in range(ksteps):
+        step(k)
+    e1.record(s_out)
+    torch.cuda.synchronize()
+    return max_fn(e0.elapsed_time(e1) * 1e-3) / ksteps
+
+
 def cpu_baseline(R, m, max_seconds=20.0):
     """The reference's CPU path on the host: reference plan() + CPU delivery.
 
@@ -255,29 +303,16 @@ def run_local(args):
     e2e = None
     if not args.no_e2e:
         hs = [torch.empty(t.numel(), dtype=torch.uint8, pin_memory=True) for t in sends]
-        hr = [torch.empty(t.numel(), dtype=torch.uint8, pin_memory=True) for t in recvs]
         for h, t in zip(hs, sends):
             h.copy_(t)
-        ksteps = max(3, min(args.steps, 10))
-
-        def e2e_step():
-            for h, t in zip(hs, sends):
-                t.copy_(h, non_blocking=True)
-            C.exchange_local(sends, recvs, m, args.ctas, stream)
-            for h, t in zip(hr, recvs):
-                h.copy_(t, non_blocking=True)
-
-        e2e_step()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(ksteps):
-            e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        te = e0.elapsed_time(e1) * 1e-3 / ksteps
+        dev = [(sends, recvs), ([torch.empty_like(t) for t in sends], [torch.empty_like(t) for t in recvs])]
+        hr = [[torch.empty(t.numel(), dtype=torch.uint8, pin_memory=True) for t in recvs] for _ in dev]
+        slots = [(list(zip(ds, hs)), list(zip(hr[j], dr))) for j, (ds, dr) in enumerate(dev)]
+        ksteps = max(4, min(args.steps, 10))
+        te = pipelined_e2e(ksteps, slots, lambda j, st: C.exchange_local(dev[j][0], dev[j][1], m, args.ctas, st))
         e2e = {"value": total / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": sum(t.numel() for t in sends),
-               "d2h_bytes_per_step": sum(t.numel() for t in recvs), "steps": ksteps}
+               "d2h_bytes_per_step": sum(t.numel() for t in recvs), "steps": ksteps,
+               "pipeline": "2 device slots; H2D / exchange / D2H on 3 streams, step k+1 H2D overlaps step k D2H"}
 
     peak, peak_src = measured_peaks()
     kernel_s = sum(per_step) / len(per_step)
@@ -392,27 +427,20 @@ def run_multi(args):
     e2e = None
     if not args.no_e2e:
         hs = torch.empty(send.numel(), dtype=torch.uint8, pin_memory=True)
-        hr = torch.empty(recv.numel(), dtype=torch.uint8, pin_memory=True)
         hs.copy_(send)
-        ksteps = max(3, min(args.steps, 10))
-
-        def e2e_step():
-            send.copy_(hs, non_blocking=True)
-            comm.alltoallv(send, sc, sd, recv, rc, rd, stream)
-            hr.copy_(recv, non_blocking=True)
-
-        e2e_step()
-        torch.cuda.synchronize()
-        barrier()
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        for _ in range(ksteps):
-            e2e_step()
-        a1.record(stream)
-        torch.cuda.synchronize()
-        te = max_over_ranks(a0.elapsed_time(a1) * 1e-3) / ksteps
+        send2, recv2 = torch.empty_like(send), torch.empty_like(recv)
+        extra = [comm.register(send2), comm.register(recv2)]
+        dev = [(send, recv), (send2, recv2)]
+        hr = [torch.empty(recv.numel(), dtype=torch.uint8, pin_memory=True) for _ in dev]
+        slots = [([(ds, hs)], [(hr[j], dr)]) for j, (ds, dr) in enumerate(dev)]
+        ksteps = max(4, min(args.steps, 10))
+        te = pipelined_e2e(ksteps, slots, lambda j, st: comm.alltoallv(dev[j][0], sc, sd, dev[j][1], rc, rd, st),
+                           max_over_ranks)
+        for h in extra:
+            comm.deregister(h)
         e2e = {"value": total / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": send.numel() * R,
-               "d2h_bytes_per_step": recv.numel() * R, "steps": ksteps, "note": "bytes summed over ranks"}
+               "d2h_bytes_per_step": recv.numel() * R, "steps": ksteps, "note": "bytes summed over ranks",
+               "pipeline": "2 device slots; H2D / exchange / D2H on 3 streams, step k+1 H2D overlaps step k D2H"}
 
     comm.deregister(handle)
     comm.deregister(shandle)
