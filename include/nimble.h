@@ -162,6 +162,10 @@ nimbleResult_t nimblePlanLinkLoads(nimblePlan_t plan, double* loads, int nlinks)
 nimbleResult_t nimblePlanMaxNormalizedLoad(nimblePlan_t plan, double* seconds);
 /* plan_to_json (planner.hpp:109) */
 nimbleResult_t nimblePlanToJson(nimblePlan_t plan, char* out, size_t cap, size_t* need);
+/* plan_from_json (planner.hpp:110): re-enumerates routes on `topo`, matches
+ * flows by (class, via, rail), checks every pair's flows sum to its demand. */
+nimbleResult_t nimblePlanFromJson(nimbleTopology_t topo, int ranks, int ranks_per_node, const char* json,
+                                  nimblePlan_t* plan);
 
 /* ------------------------------------------------------------ 2. communicator */
 

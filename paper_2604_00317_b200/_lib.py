@@ -91,6 +91,7 @@ SIGNATURES = {
     "nimblePlanLinkLoads": [c_void_p, P(c_double), c_int],
     "nimblePlanMaxNormalizedLoad": [c_void_p, P(c_double)],
     "nimblePlanToJson": [c_void_p, c_char_p, c_size, P(c_size)],
+    "nimblePlanFromJson": [c_void_p, c_int, c_int, c_char_p, P(c_void_p)],
     "nimbleCommConfigDefault": [P(CommConfig)],
     "nimbleGetUniqueId": [P(UniqueId)],
     "nimbleCommInitRank": [P(c_void_p), c_int, UniqueId, c_int],

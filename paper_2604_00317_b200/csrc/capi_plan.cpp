@@ -264,6 +264,20 @@ nimbleResult_t nimbleEnumeratePaths(nimbleTopology_t t, int ranks, int rpn, int 
     });
 }
 
+nimbleResult_t nimblePlanFromJson(nimbleTopology_t t, int ranks, int rpn, const char* json, nimblePlan_t* out) {
+    return nb::guarded([&] {
+        if (!t || !json || !out) throw std::invalid_argument("plan json: null argument");
+        auto* p = new nimblePlan{t->lm, {}};
+        try {
+            p->plan = nb::plan_from_json(t->lm, ranks, rpn, json);
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        *out = p;
+    });
+}
+
 nimbleResult_t nimblePlanDestroy(nimblePlan_t p) {
     delete p;
     return nimbleSuccess;

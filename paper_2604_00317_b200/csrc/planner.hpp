@@ -84,5 +84,8 @@ PlanResult direct_plan(const LinkModel& lm, int ranks, int rpn, const Demand& m)
 std::vector<double> link_loads(const LinkModel& lm, const PlanResult& p);
 double peak_load(const LinkModel& lm, const PlanResult& p);
 std::string plan_json(const PlanResult& p);
+// plan_from_json (planner.cpp:494-539): routes re-enumerated on `lm`, flows
+// matched by (class, via, rail), per-pair conservation checked within 0.5 B.
+PlanResult plan_from_json(const LinkModel& lm, int ranks, int rpn, const std::string& text);
 
 }  // namespace nb

@@ -300,6 +300,17 @@ def plan_to_json(p: Plan) -> dict:
     return json.loads(p.json)
 
 
+def plan_from_json(topo: Topology, ranks, ranks_per_node, doc) -> Plan:
+    """plan_from_json() -- planner.hpp:110 (accepts a dict or a JSON string)."""
+    text = doc if isinstance(doc, str) else json.dumps(doc)
+    h = c_void_p()
+    _lib.call("nimblePlanFromJson", topo.handle, ranks, ranks_per_node, text.encode(), ctypes.byref(h))
+    try:
+        return _read_plan(h, topo.link_count())
+    finally:
+        _lib.lib().nimblePlanDestroy(h)
+
+
 def port_bound_seconds(matrix, ranks, port_bytes_per_s=900e9):
     """The MCF roofline: max over GPUs of egress or ingress bytes / port rate."""
     worst = 0

@@ -1,4 +1,4 @@
-"""Multi-process host logic on CPU (gloo, world_size 2): the out-of-band
+"""Multi-process host logic on CPU (gloo, world_size 2 and 8): the out-of-band
 rendezvous nimbleCommInitRank uses, and bench.py's host-side helpers."""
 import ctypes
 import os
@@ -39,8 +39,9 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_bootstrap_and_host_helpers_two_ranks():
-    world, port = 2, _free_port()
+@pytest.mark.parametrize("world", [2, 8])
+def test_bootstrap_and_host_helpers(world):
+    port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
@@ -51,9 +52,9 @@ def test_bootstrap_and_host_helpers_two_ranks():
         p.join(timeout=60)
     for rank, rc, out, same, t in res:
         assert rc == 0
-        assert out == [0, 7, 0xABCDEF, 1, 1007, 0xABCDEF]
+        assert out == [v for r in range(world) for v in (r, r * 1000 + 7, 0xABCDEF)]
         assert same
-        assert t == pytest.approx(0.002)
+        assert t == pytest.approx(0.001 * world)
 
 
 def test_bootstrap_rejects_foreign_id(lib):

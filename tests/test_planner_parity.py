@@ -239,3 +239,28 @@ def test_port_bound_is_direct_max_load(lib):
         assert P.plan_direct_baseline(t, 8, 8, m).max_normalized_load == P.port_bound_seconds(m, 8, 900e9)
     assert P.port_bound_seconds(P.gen_skewed_a2av(8, 256 * MiB, 0.7, 0), 8) == pytest.approx(1.4615e-3, rel=1e-4)
     assert not math.isnan(P.port_bound_seconds([0, 0, 0, 0], 2))
+
+
+def test_plan_json_round_trip(lib):  # test_planner.cpp:171-191
+    t = P.build_canonical(2, 4, 4, P.gbps(120), P.gbps(50), P.ALLTOALL)
+    m = P.gen_irregular(8, 512 * MiB, 0.5, 3)
+    p = P.plan(t, 8, 4, m)
+    back = P.plan_from_json(t, 8, 4, p.json)
+    assert [pp.flows for pp in back.pairs] == [pp.flows for pp in p.pairs]
+    assert back.stats["placements"] == p.stats["placements"]
+    assert back.link_loads == p.link_loads
+    doc = P.plan_to_json(p)
+    doc["pairs"][0]["flows"][0]["bytes"] = 1.0  # break conservation
+    with pytest.raises(NimbleError):
+        P.plan_from_json(t, 8, 4, doc)
+
+
+def test_plan_from_reference_json(lib):
+    """The reference's own plan.json documents (dumped by oracle/_ref) load into
+    the product with identical flows and loads."""
+    for case in _cases.load("configs.json"):
+        req, resp = case["request"], case["response"]
+        t = _cases.topology_for(P, req)
+        back = P.plan_from_json(t, req["ranks"], _cases.rpn(req), resp["plan"])
+        assert [pp.flows for pp in back.pairs] == [[(c, b) for c, b in f] for f in _cases.ref_flows(resp)]
+        assert back.link_loads == resp["loads"]
