@@ -238,6 +238,7 @@ struct nimbleComm {
     std::list<nb::CachedSchedule> schedules;
     cudaStream_t bench_stream = nullptr;
     uint64_t* d_trace = nullptr;  // NIMBLE_TRACE=1: device timeline of the last launch
+    cudaEvent_t last_launch = nullptr;  // launches on one comm are serialized across streams
 };
 
 namespace nb {
@@ -259,7 +260,7 @@ void upload_view(nimbleComm* c) {
     c->view.status = c->d_status;
     c->view.scratch = c->d_scratch;
     const char* t = std::getenv("NIMBLE_TIMEOUT_MS");
-    c->view.timeout_ms = t && *t ? static_cast<uint32_t>(std::atoi(t)) : 20000u;
+    c->view.timeout_ms = t && *t ? static_cast<uint32_t>(std::atoi(t)) : 60000u;
     CUDA_TRY(cudaMemcpy(c->d_view, &c->view, sizeof c->view, cudaMemcpyHostToDevice));
 }
 
@@ -343,6 +344,7 @@ void setup_common(nimbleComm* c) {
     std::memset(c->h_status, 0, 64);
     CUDA_TRY(cudaHostGetDevicePointer(&c->d_status, c->h_status, 0));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->bench_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->last_launch, cudaEventDisableTiming));
     if (const char* t = std::getenv("NIMBLE_TRACE"); t && *t == '1')
         CUDA_TRY(cudaMalloc(&c->d_trace, sizeof(uint64_t) * kTraceSlots));
     c->win_table.assign(static_cast<size_t>(kMaxWindows) * kMaxRanks, 0);
@@ -584,8 +586,11 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     // small exchanges: no more CTAs than items (each CTA costs a fence at exit)
     ctas = std::max(1, std::min({ctas, c->sms, static_cast<int>(std::max<size_t>(cs.sc.items.size(), 1))}));
     // every rank launches even with nothing to move: its posts and done
-    // flags are what its peers wait for
+    // flags are what its peers wait for.  Launches of one comm share its
+    // scratch and flags, so a launch on another stream waits for the last one.
+    CUDA_TRY(cudaStreamWaitEvent(st, c->last_launch, 0));
     CUDA_TRY(launch_exchange(a, ctas, st));
+    CUDA_TRY(cudaEventRecord(c->last_launch, st));
 }
 
 void run_exchanges(std::vector<Exchange>& exs) {
@@ -928,6 +933,7 @@ nimbleResult_t nimbleCommDestroy(nimbleComm_t c) {
             if (c->d_trace) cudaFree(c->d_trace);
             cudaFreeHost(c->h_status);
             if (c->bench_stream) cudaStreamDestroy(c->bench_stream);
+            if (c->last_launch) cudaEventDestroy(c->last_launch);
         }
         if (c->clique) {
             auto& v = c->clique->comms;
