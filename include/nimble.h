@@ -191,9 +191,10 @@ typedef struct {
     int ctas;                     /* forwarding-engine CTAs per launch, 0 = auto        */
     uint64_t direct_chunk;        /* work-item size of direct pushes/pulls, self rings and
                                      local copies (<= pipe_chunk), 0 = auto (128 KiB)      */
-    int pull;                     /* receiver-driven pulls: 2 = always when the sender's
-                                     segment is registered (default), 1 = never (push),
-                                     0 = auto (only ranks with ingress > 1.25 x egress) */
+    int pull;                     /* receiver-driven pulls.  0 = auto (default): receivers
+                                     ask; a registered sender grants unless its own port is
+                                     ingress-bound (ingress > 1.55 x egress), in which case it
+                                     pushes out; 1 = never (push only); 2 = always grant */
 } nimbleCommConfig;
 
 nimbleResult_t nimbleCommConfigDefault(nimbleCommConfig* cfg);

@@ -293,7 +293,7 @@ void default_config(nimbleCommConfig* cfg, int nranks) {
     cfg->channels_per_peer = 1;
     cfg->ctas = 0;
     cfg->direct_chunk = 0;
-    cfg->pull = 2;
+    cfg->pull = 0;
 }
 
 // Allocate ctrl + staging, exchange handles / pointers, map peers.
@@ -469,9 +469,18 @@ void fill_posts(nimbleComm* c, RankBuffers& rb, const PlanResult& plan) {
     uint64_t ingress = 0, egress = 0;
     for (int p = 0; p < rb.R; ++p)
         if (p != rb.me) ingress += rb.recv_bytes[p], egress += rb.send_bytes[p];
-    // auto: only a clearly ingress-heavy rank pulls; measured on 4xB200, mixing
-    // push and pull on one port costs more than it saves, so the default is 2
-    rb.pull = c->cfg.pull == 2 || (c->cfg.pull == 0 && ingress > egress + egress / 4);
+    // Push or pull, per port, from this rank's own row and column (measured on
+    // 2-4 B200s, profiles/r01_summary.md, r01_pull_policy.md):
+    //  - a pull loads the *sender's* ingress with read requests (24 B per
+    //    128 B); a push loads the receiver's egress with almost nothing;
+    //  - pull responses carry 16 B of protocol per 128 B, writes 24 B;
+    //  - mixing pushes and pulls on links busy both ways is slow.
+    // Receivers always ask to pull; a sender declines -- and pushes its data
+    // out -- only when its own port is clearly ingress-bound (ingress > 1.55 x
+    // egress: the crossover measured on 2 and 3 GPUs), so the hot port of a
+    // skewed exchange pulls everything in and pushes everything out.
+    rb.pull = c->cfg.pull != 1;
+    const bool grant = c->cfg.pull == 2 || (c->cfg.pull == 0 && ingress * 20 <= egress * 31);
     rb.send_post.assign(static_cast<size_t>(rb.R), Post{});
     for (int d = 0; d < rb.R; ++d) {
         if (d == rb.me || rb.send_bytes[d] == 0) continue;
@@ -480,7 +489,7 @@ void fill_posts(nimbleComm* c, RankBuffers& rb, const PlanResult& plan) {
         p.bytes = rb.send_bytes[d];
         p.mode = kSendPlain;
         const int w = window_of(c, rb.send_ptr[d], rb.send_bytes[d]);
-        if (w >= 0) {
+        if (w >= 0 && grant) {
             p.mode = kSendRegistered;
             p.win = static_cast<uint32_t>(w);
             p.off = rb.send_ptr[d] - c->windows[static_cast<size_t>(w)].base;
