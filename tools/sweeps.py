@@ -108,9 +108,11 @@ def main():
         comm.set_config(pull=int(os.environ["SWEEP_PULL"]))
     R = world
     cases = os.environ.get("SWEEP_CASES", "c3,c5,c4,c1,c2").split(",")
+    per_rank = int(os.environ.get("SWEEP_PER_RANK_MIB", "256")) * MiB
     if "c3" in cases:
         for i in range(10):
-            run_point(comm, pg, rank, R, P.gen_skewed_a2av(R, 256 * MiB, i / 10, 0), "c3", extra={"ratio": i / 10})
+            run_point(comm, pg, rank, R, P.gen_skewed_a2av(R, per_rank, i / 10, 0), "c3",
+                      extra={"ratio": i / 10, "per_rank": per_rank})
     if "c5" in cases:
         run_point(comm, pg, rank, R, P.gen_skewed_a2av(R, 256 * MiB, 1.0 / (R - 1), 0), "c5")
     if "c4" in cases:
