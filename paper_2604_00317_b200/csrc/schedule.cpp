@@ -110,8 +110,9 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
                         proto.kind = kPull;
                         proto.peer = static_cast<uint8_t>(s);
                         const size_t first = keyed.size();
-                        cut(keyed, proto, 1, rb.recv_ptr[s] + off, bytes, dchunk, 0.0);
-                        for (size_t i = first; i < keyed.size(); ++i) keyed[i].item.src = off + static_cast<uint64_t>(keyed[i].item.seq) * dchunk;
+                        cut(keyed, proto, 0, rb.recv_ptr[s] + off, bytes, dchunk, 0.0);
+                        for (size_t i = first; i < keyed.size(); ++i)  // source: offset inside the sender's segment
+                            keyed[i].item.src = keyed[i].item.dst - rb.recv_ptr[s];
                         sc.pull_items[s] += static_cast<uint32_t>(keyed.size() - first);
                     }
                     if ((rb.recv_post[s].mode & 0xf) == kPostStaged) {  // drain my self ring (s, me)
