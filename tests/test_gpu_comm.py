@@ -223,6 +223,32 @@ def w_mismatch(comm, rank, R):
     return comm.async_error()
 
 
+def w_moe(comm, rank, R):
+    """MoE dispatch/combine over the nimble all-to-allv (upstream caller):
+    skewed router, expert fn = scale by (global expert id + 1), router-weighted
+    combine, compared with the same computation done locally."""
+    from paper_2604_00317_b200.moe import MoEDispatcher
+    g = torch.Generator(device="cuda").manual_seed(100 + rank)
+    T, H, k, E = 777, 96, 2, 4 * R
+    x = torch.randn(T, H, device="cuda", generator=g)
+    hot = torch.rand(T, k, device="cuda", generator=g) < 0.6
+    ids = torch.where(hot, torch.zeros_like(hot, dtype=torch.int64),
+                      torch.randint(0, E, (T, k), device="cuda", generator=g))
+    w = torch.rand(T, k, device="cuda", generator=g)
+    disp = MoEDispatcher(comm, E, H, dtype=torch.float32, max_tokens=1024, topk=k)
+    try:
+        recv_x, recv_e, h = disp.dispatch(x, ids)
+        y = recv_x * (recv_e.to(torch.float32) + rank * disp.experts_per_rank + 1).unsqueeze(1)
+        out = disp.combine(y, h, w)
+        torch.cuda.synchronize()
+        comm.check_async()
+        ref = (x.unsqueeze(1) * (ids.to(torch.float32) + 1).unsqueeze(2) * w.unsqueeze(2)).sum(1)
+        ok = torch.allclose(out, ref, rtol=1e-5, atol=1e-5)
+        return bool(ok), sum(h.recv_counts)
+    finally:
+        disp.close()
+
+
 def w_bench(comm, rank, R):
     return comm.bench_skewed(32 * MiB, 0.7, 0, warmup=1, iters=3)
 
@@ -286,6 +312,14 @@ def test_count_mismatch_is_an_error_not_a_hang():
     R = min(_ngpus(), 4)
     res = _spawn("w_mismatch", R)
     assert any(v not in (0, "0") for v in res.values()), res
+
+
+@need2
+def test_moe_dispatch_combine():
+    R = min(_ngpus(), 4)
+    res = _spawn("w_moe", R)
+    assert all(ok for ok, _ in res.values()), res
+    assert res[0][1] > max(n for _, n in list(res.values())[1:])  # rank 0 holds the hot expert
 
 
 @need2

@@ -113,6 +113,10 @@ def main():
         for i in range(10):
             run_point(comm, pg, rank, R, P.gen_skewed_a2av(R, per_rank, i / 10, 0), "c3",
                       extra={"ratio": i / 10, "per_rank": per_rank})
+    if "c3a" in cases:  # the same skew with every pair rounded down to 256 B (NCCL's aligned fast path)
+        for i in (0, 3, 5, 7, 9):
+            m = [v // 256 * 256 for v in P.gen_skewed_a2av(R, per_rank, i / 10, 0)]
+            run_point(comm, pg, rank, R, m, "c3a", extra={"ratio": i / 10, "per_rank": per_rank})
     if "c5" in cases:
         run_point(comm, pg, rank, R, P.gen_skewed_a2av(R, 256 * MiB, 1.0 / (R - 1), 0), "c5")
     if "c4" in cases:
