@@ -227,18 +227,20 @@ struct nimbleComm {
     nb::CommDevice view{};
     nb::CommDevice* d_view = nullptr;
     uint64_t* d_win_table = nullptr;
+    uint64_t* d_epoch = nullptr;
     uint32_t* d_scratch = nullptr;
     uint32_t* h_status = nullptr;  // host-mapped async error word
     uint32_t* d_status = nullptr;  // its device alias
     std::vector<nb::Window> windows;
     std::vector<uint64_t> win_table;  // [win * kMaxRanks + rank]
-    uint64_t epoch = 0;
     uint64_t plan_ids = 0;
     std::list<nb::CachedPlan> plans;
     std::list<nb::CachedSchedule> schedules;
     cudaStream_t bench_stream = nullptr;
     uint64_t* d_trace = nullptr;  // NIMBLE_TRACE=1: device timeline of the last launch
     cudaEvent_t last_launch = nullptr;  // launches on one comm are serialized across streams
+    cudaStream_t last_stream = nullptr;
+    bool launched = false;
 };
 
 namespace nb {
@@ -259,6 +261,7 @@ void upload_view(nimbleComm* c) {
     c->view.nwin = static_cast<uint32_t>(c->windows.size());
     c->view.status = c->d_status;
     c->view.scratch = c->d_scratch;
+    c->view.epoch = c->d_epoch;
     const char* t = std::getenv("NIMBLE_TIMEOUT_MS");
     c->view.timeout_ms = t && *t ? static_cast<uint32_t>(std::atoi(t)) : 60000u;
     CUDA_TRY(cudaMemcpy(c->d_view, &c->view, sizeof c->view, cudaMemcpyHostToDevice));
@@ -338,6 +341,8 @@ void setup_common(nimbleComm* c) {
     CUDA_TRY(cudaMalloc(&c->d_view, sizeof(CommDevice)));
     CUDA_TRY(cudaMalloc(&c->d_win_table, sizeof(uint64_t) * kMaxWindows * kMaxRanks));
     CUDA_TRY(cudaMemset(c->d_win_table, 0, sizeof(uint64_t) * kMaxWindows * kMaxRanks));
+    CUDA_TRY(cudaMalloc(&c->d_epoch, sizeof(uint64_t)));
+    CUDA_TRY(cudaMemset(c->d_epoch, 0, sizeof(uint64_t)));
     CUDA_TRY(cudaMalloc(&c->d_scratch, sizeof(uint32_t) * (2 + 2 * kMaxRanks)));
     CUDA_TRY(cudaMemset(c->d_scratch, 0, sizeof(uint32_t) * (2 + 2 * kMaxRanks)));
     CUDA_TRY(cudaHostAlloc(&c->h_status, 64, cudaHostAllocMapped | cudaHostAllocPortable));
@@ -540,6 +545,11 @@ CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& 
             c->schedules.splice(c->schedules.begin(), c->schedules, it);
             return c->schedules.front();
         }
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaStreamIsCapturing(st, &cap));
+    if (cap != cudaStreamCaptureStatusNone)
+        throw Error(nimbleInvalidUsage, "graph capture: run the same exchange once before capturing it "
+                                        "(its schedule must be cached; capture does not allow uploads)");
     CachedSchedule cs;
     cs.key = key;
     const char* env = std::getenv("NIMBLE_DIRECT_CHUNK");
@@ -570,7 +580,7 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     a.nitems = static_cast<uint32_t>(cs.sc.items.size());
     a.slots = slot_count(c->cfg);
     a.pipe_chunk = c->cfg.pipe_chunk;
-    a.epoch = ++c->epoch;
+    a.epoch = 0;  // the kernel takes it from c->view.epoch (device), see engine.cu
     a.comm = c->d_view;
     a.posts = cs.posts.p;
     a.send_posts = cs.send_posts.p;
@@ -597,9 +607,19 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     // every rank launches even with nothing to move: its posts and done
     // flags are what its peers wait for.  Launches of one comm share its
     // scratch and flags, so a launch on another stream waits for the last one.
-    CUDA_TRY(cudaStreamWaitEvent(st, c->last_launch, 0));
+    // A launch on another stream than the previous one first waits for it
+    // (same-stream launches are ordered already).  Not inside graph capture:
+    // a captured launch is ordered by the graph the user builds.
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaStreamIsCapturing(st, &cap));
+    const bool eager = cap == cudaStreamCaptureStatusNone;
+    if (eager && c->launched && st != c->last_stream) CUDA_TRY(cudaStreamWaitEvent(st, c->last_launch, 0));
     CUDA_TRY(launch_exchange(a, ctas, st));
-    CUDA_TRY(cudaEventRecord(c->last_launch, st));
+    if (eager) {
+        CUDA_TRY(cudaEventRecord(c->last_launch, st));
+        c->last_stream = st;
+        c->launched = true;
+    }
 }
 
 void run_exchanges(std::vector<Exchange>& exs) {
@@ -939,6 +959,7 @@ nimbleResult_t nimbleCommDestroy(nimbleComm_t c) {
             cudaFree(c->d_view);
             cudaFree(c->d_win_table);
             cudaFree(c->d_scratch);
+            cudaFree(c->d_epoch);
             if (c->d_trace) cudaFree(c->d_trace);
             cudaFreeHost(c->h_status);
             if (c->bench_stream) cudaStreamDestroy(c->bench_stream);
@@ -1009,8 +1030,8 @@ nimbleResult_t nimbleCommSetConfig(nimbleComm_t c, const nimbleCommConfig* cfg) 
             cudaFree(c->ctrl);
             c->cfg = next;
             nb::setup_regions(c, false);
+            CUDA_TRY(cudaMemset(c->d_epoch, 0, sizeof(uint64_t)));  // fresh flags: epochs restart
             nb::upload_view(c);
-            c->epoch = 0;
         }
         c->cfg = next;
         c->plans.clear();

@@ -112,6 +112,7 @@ struct CommDevice {
     uint32_t nwin;
     uint32_t timeout_ms;
     uint32_t* status;             // host-mapped: [0] error code, [1] detail
+    uint64_t* epoch;              // launches completed on this comm (advanced by each launch's last CTA)
     uint32_t* scratch;            // [0] queue head, [1] CTAs done, [2, 2+kMaxRanks) grant decisions
                                   // as sender, [2+kMaxRanks, 2+2*kMaxRanks) as receiver (kDecide*)
 };
@@ -122,7 +123,7 @@ struct LaunchArgs {
     uint32_t nitems;
     uint32_t slots;        // S
     uint64_t pipe_chunk;   // ring slot bytes
-    uint64_t epoch;
+    uint64_t epoch;        // set by the kernel itself from CommDevice::epoch (graph-replay safe)
     const CommDevice* comm;
     const Post* posts;       // [R] my receive posts for this call (device copy)
     const Post* send_posts;  // [R] my send posts for this call (device copy)

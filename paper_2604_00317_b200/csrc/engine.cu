@@ -561,9 +561,17 @@ constexpr size_t kEngineSmem = sizeof(SharedState) + 128 + static_cast<size_t>(k
 
 }  // namespace
 
-__global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_constant__ LaunchArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_constant__ LaunchArgs args) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     SharedState& sh = *reinterpret_cast<SharedState*>(smem_raw);
+    // The launch's epoch comes from device memory, not the host: a launch
+    // captured in a CUDA graph and replayed gets a fresh epoch every time.
+    __shared__ LaunchArgs a;
+    if (threadIdx.x == 0) {
+        a = args;
+        a.epoch = args.local_only ? 0 : *reinterpret_cast<volatile uint64_t*>(args.comm->epoch) + 1;
+    }
+    __syncthreads();
     uint8_t* stages = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw + sizeof(SharedState)) + 127) & ~static_cast<uintptr_t>(127));
     const CommDevice* c = a.comm;
@@ -654,6 +662,7 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
         __syncwarp();
         if (lane == 0) {
             trace_max(a, kTraceWaited);
+            if (!a.local_only) *c->epoch = a.epoch;
             scratch[0] = 0;
             __threadfence();
             scratch[1] = 0;
