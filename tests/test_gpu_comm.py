@@ -370,3 +370,50 @@ def test_bench_entry_point():
     R = min(_ngpus(), 4)
     for r, b in _spawn("w_bench", R).items():
         assert b["mismatches"] == 0 and b["gbps_effective"] > 0 and b["bound_seconds"] > 0
+
+
+@need2
+def test_comm_init_all_single_process_grouped():
+    """nimbleCommInitAll: every GPU in this process, one grouped call per step
+    (NCCL's single-process pattern), registered and unregistered receives,
+    mesh model (row allgather inside the clique) included."""
+    from paper_2604_00317_b200 import comm as C
+    from paper_2604_00317_b200 import planner as P
+    R = min(_ngpus(), 4)
+    comms = C.Comm.init_all(list(range(R)))
+    try:
+        for fabric, register in (("nvswitch", True), ("nvswitch", False), ("alltoall", True)):
+            for c in comms:
+                with torch.cuda.device(c.device):
+                    c.set_config(fabric=fabric, gpus_per_node=R)
+            m = P.gen_p2p(R, 0, 1, 96 * MiB) if fabric == "alltoall" else P.gen_skewed_a2av(R, 3 * MiB + 1, 0.7, 0)
+            bufs = []
+            for c in comms:
+                with torch.cuda.device(c.device):
+                    sc, sd, rc, rd = C.packed_displs(m, R, c.rank)
+                    send = torch.empty(max(sum(sc), 16), dtype=torch.uint8, device="cuda")
+                    recv = torch.zeros(max(sum(rc), 16), dtype=torch.uint8, device="cuda")
+                    for d in range(R):
+                        C.fill_payload(send[sd[d]:], 0, sc[d], 77, c.rank, d)
+                    torch.cuda.synchronize()
+                    hs = [c.register(send), c.register(recv)] if register else []
+                    bufs.append((c, send, recv, sc, sd, rc, rd, hs))
+            with C.group():
+                for c, send, recv, sc, sd, rc, rd, hs in bufs:
+                    with torch.cuda.device(c.device):
+                        c.alltoallv(send, sc, sd, recv, rc, rd)
+            for c, send, recv, sc, sd, rc, rd, hs in bufs:
+                with torch.cuda.device(c.device):
+                    torch.cuda.synchronize()
+                    c.check_async()
+                    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+                    for s in range(R):
+                        C.check_payload(recv[rd[s]:], 0, rc[s], 77, s, c.rank, bad)
+                    torch.cuda.synchronize()
+                    assert int(bad.item()) == 0, (fabric, register, c.rank)
+                    for h in hs:
+                        c.deregister(h)
+    finally:
+        for c in comms:
+            with torch.cuda.device(c.device):
+                c.destroy()

@@ -166,3 +166,22 @@ def test_payload_fill_matches_oracle():
         want = np.zeros(n, dtype=np.uint8)
         ref.cpu_lib().orc_fill(want.ctypes.data, first, n, 77, 3, 5)
         assert np.array_equal(t.cpu().numpy(), want)
+
+
+def test_comm_config_validation():
+    from paper_2604_00317_b200 import comm as C
+    from paper_2604_00317_b200._lib import NimbleError
+    c = C.Comm.init_rank(1, C.unique_id(), 0)
+    try:
+        cfg = c.config()
+        assert cfg.fabric == 1 and cfg.pipe_chunk == 64 << 10 and cfg.p2p_buffer == 10 << 20 and cfg.pull == 0
+        with pytest.raises(NimbleError):
+            c.set_config(fabric="alltoall", gpus_per_node=4)      # mesh model needs one GPU per rank
+        with pytest.raises(NimbleError):
+            c.set_config(pipe_chunk=64 << 10, p2p_buffer=32 << 20)  # 512 slots > 256
+        with pytest.raises(NimbleError):
+            c.set_config(pipe_chunk=1 << 20, p2p_buffer=512 << 10)  # buffer holds no chunk
+        c.set_config(pipe_chunk=512 << 10, p2p_buffer=10 << 20)     # the reference's geometry is valid
+        assert c.config().pipe_chunk == 512 << 10
+    finally:
+        c.destroy()
