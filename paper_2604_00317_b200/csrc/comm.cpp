@@ -782,11 +782,32 @@ void bench_matrix(nimbleComm* c, const std::vector<uint64_t>& m, int warmup, int
         rd[p] = rtot;
         rtot += rc[p];
     }
-    uint8_t *sbuf = nullptr, *rbuf = nullptr;
-    uint64_t* bad = nullptr;
-    CUDA_TRY(cudaMalloc(&sbuf, std::max<size_t>(stot, 16)));
-    CUDA_TRY(cudaMalloc(&rbuf, std::max<size_t>(rtot, 16)));
-    CUDA_TRY(cudaMalloc(&bad, sizeof(uint64_t)));
+    // Buffers and windows are released on every exit path (the windows' IPC
+    // mappings are dropped locally; the comm's peers do the same on theirs).
+    struct Scope {
+        nimbleComm* c;
+        std::vector<void*> bufs;
+        size_t first_window;
+        ~Scope() {
+            cudaStreamSynchronize(c->bench_stream);
+            for (size_t k = first_window; k < c->windows.size(); ++k) {
+                c->windows[k].live = false;
+                for (void* p : c->windows[k].opened) ipc_cache().release(p);
+                c->windows[k].opened.clear();
+            }
+            c->schedules.clear();
+            for (void* b : bufs) cudaFree(b);
+        }
+    } scope{c, {}, c->windows.size()};
+    auto alloc = [&scope](size_t n) {
+        void* p = nullptr;
+        CUDA_TRY(cudaMalloc(&p, n));
+        scope.bufs.push_back(p);
+        return p;
+    };
+    auto* sbuf = static_cast<uint8_t*>(alloc(std::max<size_t>(stot, 16)));
+    auto* rbuf = static_cast<uint8_t*>(alloc(std::max<size_t>(rtot, 16)));
+    auto* bad = static_cast<uint64_t*>(alloc(sizeof(uint64_t)));
     const uint64_t seed = 1;
     cudaStream_t st = c->bench_stream;
     for (int p = 0; p < R; ++p) CUDA_TRY(launch_fill(sbuf + sd[p], 0, sc[p], seed, me, p, st));
@@ -859,16 +880,7 @@ void bench_matrix(nimbleComm* c, const std::vector<uint64_t>& m, int warmup, int
         for (const PairRoutes& p : pr.pairs)
             for (const Flow& f : p.flows) out->relay_flows += p.cands[static_cast<size_t>(f.cand)].via >= 0;
     }
-    c->boot->barrier();
-    for (size_t k = c->windows.size() - 2; k < c->windows.size(); ++k) {
-        c->windows[k].live = false;
-        for (void* p : c->windows[k].opened) ipc_cache().release(p);
-        c->windows[k].opened.clear();
-    }
-    c->schedules.clear();
-    cudaFree(sbuf);
-    cudaFree(rbuf);
-    cudaFree(bad);
+    c->boot->barrier();  // no peer touches these windows any more
 }
 
 }  // namespace
