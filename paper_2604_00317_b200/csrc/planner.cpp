@@ -112,6 +112,9 @@ class Refiner {
             std::vector<std::vector<double>>& acc, LoadBook& book, const PlanParams& p)
         : pairs_(pairs), acc_(acc), book_(book), p_(p), eps_(static_cast<double>(p.epsilon)) {
         (void)lm;
+        pens_.resize(pairs.size());
+        for (size_t i = 0; i < pairs.size(); ++i)
+            for (const Candidate& c : pairs[i].cands) pens_[i].push_back(p.cost.penalty(c, pairs[i].demand));
     }
 
     std::uint64_t run() {
@@ -132,6 +135,7 @@ class Refiner {
     LoadBook& book_;
     const PlanParams& p_;
     const double eps_;
+    std::vector<std::vector<double>> pens_;  // hop penalty per (pair, route): constant during refinement
     std::uint64_t moves_ = 0;
     int ejects_ = 0;
 
@@ -141,7 +145,7 @@ class Refiner {
         acc_[i][from] -= q;
         acc_[i][to] += q;
     }
-    double pen(size_t i, size_t c) const { return p_.cost.penalty(pairs_[i].cands[c], pairs_[i].demand); }
+    double pen(size_t i, size_t c) const { return pens_[i][c]; }
 
     bool reduce() {
         bool any = false;
