@@ -26,6 +26,7 @@ CASES = [
 def main():
     rows = ["# Planner latency (round 1)", "",
             "- Protocol: `plan()` with 5 warm-up calls, then the median of 100 timed calls, on one host core.",
+            "- Each side is repeated 5 times, interleaved, and the best median is kept (the host is shared).",
             "- Reference: its own `PlanStats.wall_seconds` (`planner.cpp:325,426`) through oracle/_ref.",
             "- Product: `nimblePlanCreate`, also timed by `PlanStats.wall_seconds`.",
             "- Both use the same matrix and produce the same (bit-exact) plan.", "",
@@ -34,12 +35,13 @@ def main():
         m = gen()
         req = {"ranks": R, "topology": {"nodes": 1, "gpus": R, "nics": 0, "fabric": fab, "nvlink_gbps": 900.0,
                                         "rail_gbps": 50.0}, "workload": {"kind": "matrix", "bytes": m}}
-        t_ref = ref.time_plan(req, 5, 100)
         topo = P.build_canonical(1, R, 0, 900e9, 0, fab)
-        for _ in range(5):
-            P.plan(topo, R, R, m)
-        ts = [P.plan(topo, R, R, m).stats["wall_seconds"] for _ in range(100)]
-        t_prod = statistics.median(ts)
+        t_ref, t_prod = float("inf"), float("inf")
+        for _ in range(5):  # interleaved repeats, best median of each: the host is shared and noisy
+            t_ref = min(t_ref, ref.time_plan(req, 5, 100))
+            for _ in range(5):
+                P.plan(topo, R, R, m)
+            t_prod = min(t_prod, statistics.median(P.plan(topo, R, R, m).stats["wall_seconds"] for _ in range(100)))
         rows.append(f"| {name} | {t_ref * 1e3:.4f} | {t_prod * 1e3:.4f} | {t_ref / t_prod:.2f}x |")
         print(rows[-1], flush=True)
     with open(os.path.join(ROOT, "profiles", "r01_planner_latency.md"), "w") as f:
