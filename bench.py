@@ -308,7 +308,7 @@ def run_local(args):
         dev = [(sends, recvs), ([torch.empty_like(t) for t in sends], [torch.empty_like(t) for t in recvs])]
         hr = [[torch.empty(t.numel(), dtype=torch.uint8, pin_memory=True) for t in recvs] for _ in dev]
         slots = [(list(zip(ds, hs)), list(zip(hr[j], dr))) for j, (ds, dr) in enumerate(dev)]
-        ksteps = max(4, min(args.steps, 10))
+        ksteps = min(max(args.steps, 20), 50)
         te = pipelined_e2e(ksteps, slots, lambda j, st: C.exchange_local(dev[j][0], dev[j][1], m, args.ctas, st))
         e2e = {"value": total / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": sum(t.numel() for t in sends),
                "d2h_bytes_per_step": sum(t.numel() for t in recvs), "steps": ksteps,
@@ -433,13 +433,15 @@ def run_multi(args):
         dev = [(send, recv), (send2, recv2)]
         hr = [torch.empty(recv.numel(), dtype=torch.uint8, pin_memory=True) for _ in dev]
         slots = [([(ds, hs)], [(hr[j], dr)]) for j, (ds, dr) in enumerate(dev)]
-        ksteps = max(4, min(args.steps, 10))
+        ksteps = min(max(args.steps, 20), 50)
         te = pipelined_e2e(ksteps, slots, lambda j, st: comm.alltoallv(dev[j][0], sc, sd, dev[j][1], rc, rd, st),
                            max_over_ranks)
         for h in extra:
             comm.deregister(h)
-        e2e = {"value": total / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": send.numel() * R,
-               "d2h_bytes_per_step": recv.numel() * R, "steps": ksteps, "note": "bytes summed over ranks",
+        io = torch.tensor([float(send.numel()), float(recv.numel())], dtype=torch.float64)
+        dist.all_reduce(io)
+        e2e = {"value": total / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": int(io[0]),
+               "d2h_bytes_per_step": int(io[1]), "steps": ksteps, "note": "bytes summed over ranks",
                "pipeline": "2 device slots; H2D / exchange / D2H on 3 streams, step k+1 H2D overlaps step k D2H"}
 
     comm.deregister(handle)

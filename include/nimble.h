@@ -189,12 +189,17 @@ typedef struct {
                                      slots = channels * p2p_buffer / pipe_chunk <= 256  */
     int channels_per_peer;        /* rings per relayed flow, 1 (pipeline.hpp:23)        */
     int ctas;                     /* forwarding-engine CTAs per launch, 0 = auto        */
-    uint64_t direct_chunk;        /* work-item size of direct pushes/pulls, self rings and
-                                     local copies (<= pipe_chunk), 0 = auto (128 KiB)      */
+    uint64_t direct_chunk;        /* work-item size of direct pulls, self rings and local
+                                     copies (<= pipe_chunk), 0 = auto (128 KiB, capped at
+                                     pipe_chunk)                                           */
     int pull;                     /* receiver-driven pulls.  0 = auto (default): receivers
                                      ask; a registered sender grants unless its own port is
                                      ingress-bound (ingress > 1.55 x egress), in which case it
                                      pushes out; 1 = never (push only); 2 = always grant */
+    uint64_t push_chunk;          /* work-item size of direct pushes (<= pipe_chunk), 0 = auto
+                                     (8 KiB).  A port that pulls in while it pushes out runs
+                                     both through one CTA ring; short pushes keep a store
+                                     stalled on a busy egress from holding up the pulls   */
 } nimbleCommConfig;
 
 nimbleResult_t nimbleCommConfigDefault(nimbleCommConfig* cfg);
@@ -298,7 +303,8 @@ typedef struct {
     uint32_t pad;
 } nimbleItem;
 nimbleResult_t nimbleDebugSchedule(nimblePlan_t plan, int rank, int ranks, uint64_t pipe_chunk, uint32_t slots,
-                                   uint64_t direct_chunk, uint64_t recv_staged_mask, uint64_t pull_mask,
+                                   uint64_t direct_chunk, uint64_t push_chunk, uint64_t recv_staged_mask,
+                                   uint64_t pull_mask,
                                    nimbleItem* items, int cap, int* nitems);
 
 /* Device timeline of the comm's last launch (%globaltimer ns): kernel start,

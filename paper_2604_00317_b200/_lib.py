@@ -38,7 +38,8 @@ class PlanStats(ctypes.Structure):  # nimblePlanStats
 class CommConfig(ctypes.Structure):  # nimbleCommConfig
     _fields_ = [("fabric", c_int), ("gpus_per_node", c_int), ("nvlink_bytes_per_s", c_double),
                 ("planner", PlannerConfig), ("pipe_chunk", c_u64), ("p2p_buffer", c_u64),
-                ("channels_per_peer", c_int), ("ctas", c_int), ("direct_chunk", c_u64), ("pull", c_int)]
+                ("channels_per_peer", c_int), ("ctas", c_int), ("direct_chunk", c_u64), ("pull", c_int),
+                ("push_chunk", c_u64)]
 
 
 class UniqueId(ctypes.Structure):  # nimbleUniqueId
@@ -122,7 +123,7 @@ SIGNATURES = {
     "nimbleBenchMatrix": [c_void_p, P(c_u64), c_int, c_int, P(BenchResult)],
     "nimbleBootstrapAllgather": [P(UniqueId), c_int, c_int, c_void_p, c_size, c_void_p],
     "nimbleCommDebugTrace": [c_void_p, P(c_u64), c_int],
-    "nimbleDebugSchedule": [c_void_p, c_int, c_int, c_u64, ctypes.c_uint32, c_u64, c_u64, c_u64, c_void_p, c_int,
+    "nimbleDebugSchedule": [c_void_p, c_int, c_int, c_u64, ctypes.c_uint32, c_u64, c_u64, c_u64, c_u64, c_void_p, c_int,
                             P(c_int)],
 }
 _RESTYPES = {"nimbleGetErrorString": c_char_p, "nimbleGetLastError": c_char_p}

@@ -354,8 +354,8 @@ nimbleResult_t nimblePlanToJson(nimblePlan_t p, char* out, size_t cap, size_t* n
 }
 
 nimbleResult_t nimbleDebugSchedule(nimblePlan_t p, int rank, int ranks, uint64_t pipe_chunk, uint32_t slots,
-                                   uint64_t direct_chunk, uint64_t staged, uint64_t pull, nimbleItem* items, int cap,
-                                   int* nitems) {
+                                   uint64_t direct_chunk, uint64_t push_chunk, uint64_t staged, uint64_t pull,
+                                   nimbleItem* items, int cap, int* nitems) {
     static_assert(sizeof(nimbleItem) == sizeof(nb::Item), "nimbleItem mirrors the engine's Item");
     return nb::guarded([&] {
         if (!p || !nitems || ranks < 1 || ranks > nb::kMaxRanks || rank < 0 || rank >= ranks)
@@ -387,7 +387,7 @@ nimbleResult_t nimbleDebugSchedule(nimblePlan_t p, int rank, int ranks, uint64_t
                 if ((pull >> q) & 1) post.mode |= nb::kPostPullRequest;
             }
         }
-        nb::Schedule sc = nb::build_schedule(p->plan, rb, pipe_chunk, slots, direct_chunk);
+        nb::Schedule sc = nb::build_schedule(p->plan, rb, pipe_chunk, slots, direct_chunk, push_chunk);
         *nitems = static_cast<int>(sc.items.size());
         if (items) std::memcpy(items, sc.items.data(), std::min<size_t>(sc.items.size(), cap > 0 ? cap : 0) * sizeof(nb::Item));
     });

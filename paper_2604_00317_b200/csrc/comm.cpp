@@ -269,6 +269,11 @@ void upload_view(nimbleComm* c) {
 
 constexpr uint32_t kMaxWindows = 256;
 constexpr uint64_t kDefaultDirectChunk = 128ull << 10;
+// Direct pushes default to 8 KiB items: on 4 B200s the skewed exchange's hot
+// port (pulling in, pushing out) gains 0.03-0.09 of the bound at hotspot
+// ratios 0.6-0.8 over 64 KiB, and push-only traffic does not lose
+// (profiles/r01_push_chunk.md).
+constexpr uint64_t kDefaultPushChunk = 8ull << 10;
 
 uint32_t slot_count(const nimbleCommConfig& cfg) {
     if (cfg.pipe_chunk == 0) throw Error(nimbleInvalidArgument, "config: pipe_chunk must be positive");
@@ -297,6 +302,7 @@ void default_config(nimbleCommConfig* cfg, int nranks) {
     cfg->ctas = 0;
     cfg->direct_chunk = 0;
     cfg->pull = 0;
+    cfg->push_chunk = 0;
 }
 
 // Allocate ctrl + staging, exchange handles / pointers, map peers.
@@ -529,7 +535,7 @@ void fill_posts(nimbleComm* c, RankBuffers& rb, const PlanResult& plan) {
 CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& plan, const RankBuffers& rb,
                              cudaStream_t st) {
     std::vector<uint64_t> key = {plan_id, c->cfg.pipe_chunk, c->cfg.p2p_buffer,
-                                 static_cast<uint64_t>(c->cfg.channels_per_peer), c->cfg.direct_chunk};
+                                 static_cast<uint64_t>(c->cfg.channels_per_peer), c->cfg.direct_chunk, c->cfg.push_chunk};
     for (int r = 0; r < rb.R; ++r) {
         key.push_back(rb.send_ptr[r]);
         key.push_back(rb.send_bytes[r]);
@@ -556,7 +562,8 @@ CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& 
     const uint64_t dchunk = c->cfg.direct_chunk ? c->cfg.direct_chunk
                             : env && *env          ? std::strtoull(env, nullptr, 0)
                                                    : kDefaultDirectChunk;
-    cs.sc = build_schedule(plan, rb, c->cfg.pipe_chunk, slot_count(c->cfg), dchunk);
+    cs.sc = build_schedule(plan, rb, c->cfg.pipe_chunk, slot_count(c->cfg), dchunk,
+                           c->cfg.push_chunk ? c->cfg.push_chunk : kDefaultPushChunk);
     if (c->schedules.size() >= 4) {  // recycle the oldest entry's device buffers
         CUDA_TRY(cudaDeviceSynchronize());  // no launch may still read them
         CachedSchedule& old = c->schedules.back();
@@ -597,7 +604,7 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     a.nfinal = static_cast<uint32_t>(cs.sc.final_waits.size() / 2);
     a.local_only = 0;
     if (c->d_trace) {
-        static const uint64_t init[kTraceSlots] = {~0ull, 0, ~0ull, 0, 0, 0, 0, 0};
+        static const uint64_t init[kTraceSlots] = {~0ull, 0, ~0ull, 0, 0, 0, 0, ~0ull};
         CUDA_TRY(cudaMemcpyAsync(c->d_trace, init, sizeof init, cudaMemcpyHostToDevice, st));
         a.trace = c->d_trace;
     }

@@ -81,11 +81,18 @@ struct WirePost {
     uint64_t w[4];
 };
 
+// Posts are pushed to their reader, who polls local memory: post_in[e][d] is
+// receiver d's post for me (the direct sender), send_post[e][s] is sender s's
+// send post for me (the receiver).  post[e][s] is my own copy of my post for
+// sender s, read remotely only by relays forwarding s's chunks to me.  Slot
+// e & 1 holds epoch e; a slot holding a newer epoch means its writer finished
+// epoch e without needing the reader (see read_post in engine.cu).
 struct CtrlHeader {
-    WirePost post[2][kMaxRanks];       // written by me (the receiver), read by writers
+    WirePost post[2][kMaxRanks];       // written by me (the receiver), read by relays
     uint64_t done[kMaxRanks];          // done[w] = epoch: writer w finished writing into me
-    WirePost send_post[2][kMaxRanks];  // written by me (the sender), read by pulling receivers
+    WirePost send_post[2][kMaxRanks];  // send_post[e][s]: pushed by sender s, read by me
     uint64_t pulled[kMaxRanks];        // pulled[d] = epoch: receiver d finished pulling from me
+    WirePost post_in[2][kMaxRanks];    // post_in[e][d]: pushed by receiver d, read by me
 };
 
 // Geometry of the flag arrays that follow the header inside ctrl.
@@ -149,6 +156,7 @@ enum TraceSlot : int {
     kTraceCtasDone = 4,      // last CTA arrived at the epilogue
     kTraceSignalled = 5,     // done / pulled published
     kTraceWaited = 6,        // all incoming completions observed
+    kTraceFirstCtaDone = 7,  // min over CTAs: first CTA out of work
     kTraceSlots = 8,
 };
 

@@ -130,6 +130,7 @@ enum AsyncCode : uint32_t {
     kErrSizeMismatch = 5,
     kErrRelayToStaged = 6,
     kErrFinalTimeout = 7,
+    kErrPostLost = 8,  // a post was overwritten in a way the protocol does not allow
 };
 
 // Producer-thread wait until *p >= tag; false (and an async error) on timeout
@@ -216,8 +217,17 @@ struct PostView {
     uint64_t off, bytes;
 };
 
-// Wait for this epoch's post at p and decode it.  False (async error) on timeout.
-__device__ bool read_post(const WirePost* p, uint64_t epoch, const CommDevice* c, PostView& out) {
+enum PostRead { kPostFailed, kPostOk, kPostAdvanced };
+
+// Wait for this epoch's post at p and decode it.  kPostFailed (async error)
+// on timeout.  With `may_advance`, a slot already holding a NEWER epoch
+// returns kPostAdvanced: the writer finished this epoch and the next one
+// without waiting for me, which the protocol allows in exactly one way per
+// post kind (resolve / resolve_send say which) -- so the overwritten post's
+// content is implied and the reader does not wait for a post that will never
+// come back.
+__device__ PostRead read_post(const WirePost* p, uint64_t epoch, const CommDevice* c, PostView& out,
+                              bool may_advance) {
     const uint64_t e32 = epoch & 0xffffffffull, e16 = epoch & 0xffffull;
     const uint64_t t0 = global_ns();
     const uint64_t limit = static_cast<uint64_t>(c->timeout_ms) * 1000000ull;
@@ -230,14 +240,16 @@ __device__ bool read_post(const WirePost* p, uint64_t epoch, const CommDevice* c
                 out.win = static_cast<uint32_t>((w0 >> 16) & 0xffff);
                 out.off = w1 & 0xffffffffffffull;
                 out.bytes = w2 & 0xffffffffffffull;
-                return true;
+                return kPostOk;
             }
+        } else if (may_advance && static_cast<int32_t>(static_cast<uint32_t>(w0 >> 32) - static_cast<uint32_t>(e32)) > 0) {
+            return kPostAdvanced;
         }
         if ((spin & 255) == 255) {
-            if (*reinterpret_cast<volatile uint32_t*>(c->status) != 0) return false;
+            if (*reinterpret_cast<volatile uint32_t*>(c->status) != 0) return kPostFailed;
             if (global_ns() - t0 > limit) {
                 atomicCAS(c->status, 0u, static_cast<uint32_t>(kErrPostTimeout));
-                return false;
+                return kPostFailed;
             }
         }
         if (spin > 64) __nanosleep(32);
@@ -254,17 +266,33 @@ __device__ __forceinline__ void write_post(WirePost* p, uint64_t epoch, const Po
 
 enum Decide : uint32_t { kDecidePull = 1, kDecidePush = 2 };  // per-launch grant records (scratch)
 
-// Resolve receiver d's post for sender s (producer thread).
+// Resolve receiver d's post for sender s (producer thread): the direct
+// sender reads the copy d pushed into its own ctrl, a relay reads d's.
 __device__ bool resolve(SharedState& sh, const LaunchArgs& a, int d, int s) {
     const int key = d * kMaxRanks + s;
     if (sh.seg_mode[key]) return true;
     const CommDevice* c = a.comm;
+    const bool direct = s == c->rank;
     PostView v;
-    if (!read_post(&reinterpret_cast<const CtrlHeader*>(c->ctrl[d])->post[a.epoch & 1][s], a.epoch, c, v))
-        return false;
+    const PostRead r = direct
+        ? read_post(&reinterpret_cast<const CtrlHeader*>(c->ctrl[s])->post_in[a.epoch & 1][d], a.epoch, c, v, true)
+        : read_post(&reinterpret_cast<const CtrlHeader*>(c->ctrl[d])->post[a.epoch & 1][s], a.epoch, c, v, false);
+    if (r == kPostFailed) return false;
+    if (r == kPostAdvanced) {
+        // d got past this epoch without waiting for me, so it did not take my
+        // push: it pulled my segment, which needs my send window registered.
+        if (a.send_posts[d].mode != kSendRegistered) {
+            atomicCAS(c->status, 0u, static_cast<uint32_t>(kErrPostLost));
+            return false;
+        }
+        sh.seg_base[key] = 0;
+        sh.seg_mode[key] = kPostZeroCopy | kPostPullRequest;
+        c->scratch[2 + d] = kDecidePull;
+        return true;
+    }
     const uint32_t mode = v.mode, win = v.win;
     const uint64_t off = v.off;
-    if (s == c->rank) {  // my own outgoing segment: sizes must agree end to end
+    if (direct) {  // my own outgoing segment: sizes must agree end to end
         const uint64_t expect = v.bytes;
         if (expect != a.send_bytes[d]) {
             atomicCAS(c->status, 0u, static_cast<uint32_t>(kErrSizeMismatch));
@@ -273,7 +301,7 @@ __device__ bool resolve(SharedState& sh, const LaunchArgs& a, int d, int s) {
     }
     sh.seg_base[key] = (mode & 0xf) == kPostZeroCopy ? c->win_table[win * kMaxRanks + d] + off : 0;
     sh.seg_mode[key] = mode;
-    if (s == c->rank)  // record, for the epilogue, whether d pulls my segment or takes pushes
+    if (direct)  // record, for the epilogue, whether d pulls my segment or takes pushes
         c->scratch[2 + d] = ((mode & kPostPullRequest) && a.send_posts[d].mode == kSendRegistered) ? kDecidePull
                                                                                                     : kDecidePush;
     return true;
@@ -284,8 +312,15 @@ __device__ bool resolve_send(SharedState& sh, const LaunchArgs& a, int s) {
     if (sh.send_mode[s]) return true;
     const CommDevice* c = a.comm;
     PostView v;
-    if (!read_post(&reinterpret_cast<const CtrlHeader*>(c->ctrl[s])->send_post[a.epoch & 1][c->rank], a.epoch, c, v))
-        return false;
+    const PostRead r =
+        read_post(&reinterpret_cast<const CtrlHeader*>(c->ctrl[c->rank])->send_post[a.epoch & 1][s], a.epoch, c, v, true);
+    if (r == kPostFailed) return false;
+    if (r == kPostAdvanced) {
+        // s got past this epoch without waiting for my pull: it pushed (declined).
+        v.mode = kSendPlain;
+        v.win = 0;
+        v.off = 0;
+    }
     const uint32_t mode = v.mode, win = v.win;
     const uint64_t off = v.off;
     c->scratch[2 + kMaxRanks + s] = mode == kSendRegistered ? kDecidePull : kDecidePush;
@@ -600,8 +635,16 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
         const int peer = send_side ? tid - R : tid;
         const Post p = send_side ? a.send_posts[peer] : a.posts[peer];
         if (p.tag) {
-            CtrlHeader* h = reinterpret_cast<CtrlHeader*>(c->ctrl[me]);
-            write_post((send_side ? h->send_post : h->post)[a.epoch & 1] + peer, a.epoch, p);
+            // pushed to the reader (it polls local memory); my own copy of a
+            // receive post serves relays
+            CtrlHeader* ph = reinterpret_cast<CtrlHeader*>(c->ctrl[peer]);
+            const int e = static_cast<int>(a.epoch & 1);
+            if (send_side) {
+                write_post(&ph->send_post[e][me], a.epoch, p);
+            } else {
+                write_post(&ph->post_in[e][me], a.epoch, p);
+                write_post(&reinterpret_cast<CtrlHeader*>(c->ctrl[me])->post[e][peer], a.epoch, p);
+            }
         }
     }
     __syncthreads();
@@ -627,6 +670,7 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
         // and local copies only read remote memory: a GPU-scope fence will do)
         if (sh.remote_writes) __threadfence_system();
         else __threadfence();
+        trace_min(a, kTraceFirstCtaDone);
         last_cta = atomicAdd(&scratch[1], 1u) + 1 == gridDim.x;
     }
     __syncthreads();

@@ -49,12 +49,13 @@ constexpr double kHop2 = 1e-9;  // forward of chunk k sorts right after its stag
 }  // namespace
 
 Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t pipe_chunk, uint32_t slots,
-                        uint64_t direct_chunk) {
+                        uint64_t direct_chunk, uint64_t push_chunk) {
     const int R = rb.R, me = rb.me;
     if (R > kMaxRanks) throw Error(nimbleInvalidArgument, "schedule: too many ranks");
     if (pipe_chunk == 0 || pipe_chunk > 0xffffffffull) throw Error(nimbleInvalidArgument, "schedule: bad pipe_chunk");
     if (slots == 0 || slots > kMaxSlots) throw Error(nimbleInvalidArgument, "schedule: bad slot count");
     const uint64_t dchunk = std::min<uint64_t>(std::max<uint64_t>(direct_chunk, 4096), pipe_chunk);
+    const uint64_t schunk = push_chunk ? std::min<uint64_t>(std::max<uint64_t>(push_chunk, 4096), pipe_chunk) : dchunk;
     Schedule sc;
     sc.posts = rb.recv_post;
     sc.send_posts = rb.send_post;
@@ -96,7 +97,7 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
                     proto.kind = kPush;
                     proto.peer = static_cast<uint8_t>(d);
                     const size_t first = keyed.size();
-                    cut(keyed, proto, rb.send_ptr[d] + off, off, bytes, dchunk, 0.0);
+                    cut(keyed, proto, rb.send_ptr[d] + off, off, bytes, schunk, 0.0);
                     sc.push_items[d] += static_cast<uint32_t>(keyed.size() - first);
                     sc.push_targets |= 1ull << d;
                     sc.write_targets |= 1ull << d;
@@ -120,7 +121,8 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
                         proto.kind = kForward;
                         proto.peer = static_cast<uint8_t>(me);
                         proto.aux = static_cast<uint16_t>(s);
-                        cut(keyed, proto, 0, off, bytes, dchunk, kHop2);
+                        // chunk k of the ring is the sender's push item k: same cut
+                        cut(keyed, proto, 0, off, bytes, schunk, kHop2);
                     } else {
                         sc.recv_zc |= 1ull << s;
                     }

@@ -49,7 +49,7 @@ struct Schedule {
 // and of local copies -- small enough that the last wave of items ends within
 // a few microseconds across CTAs.
 Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t pipe_chunk, uint32_t slots,
-                        uint64_t direct_chunk);
+                        uint64_t direct_chunk, uint64_t push_chunk = 0);
 
 // 1-GPU emulated exchange: every pair's segment as local copies (packed layout).
 std::vector<Item> build_local_items(int R, const uint64_t* matrix, const uint64_t* send_base,

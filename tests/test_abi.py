@@ -71,3 +71,35 @@ def test_sass_is_sm100a_with_tma_and_release_flags(lib):
     assert "sm_100a" in r.stdout
     for mnemonic in ("UBLKCP.S.G", "SYNCS.ARRIVE.TRANS64", "STG.E.128", "STG.E.64.STRONG.SYS"):
         assert mnemonic in r.stdout, mnemonic
+
+
+def test_ctypes_structs_match_the_header_layout(tmp_path):
+    """Every ctypes struct has the C header's size and field offsets (a C
+    program compiled against include/nimble.h prints them)."""
+    pairs = [(_lib.PlannerConfig, "nimblePlannerConfig"), (_lib.PlanStats, "nimblePlanStats"),
+             (_lib.CommConfig, "nimbleCommConfig"), (_lib.UniqueId, "nimbleUniqueId"),
+             (_lib.Item, "nimbleItem"), (_lib.BenchResult, "nimbleBenchResult")]
+    lines = ['#include <stddef.h>', '#include <stdio.h>', '#include "nimble.h"', "int main(void) {"]
+    for cls, cname in pairs:
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f in cls._fields_:
+            lines.append(f'printf("{cname} {f[0]} %zu\\n", offsetof({cname}, {f[0].rstrip("_")}));')
+    lines += ["return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(l.rsplit(" ", 1) for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                         check=True).stdout.splitlines())
+    for cls, cname in pairs:
+        assert int(got[f"{cname} size"]) == ctypes.sizeof(cls), cname
+        for f in cls._fields_:
+            assert int(got[f"{cname} {f[0]}"]) == getattr(cls, f[0]).offset, (cname, f[0])
+
+
+def test_comm_config_defaults_through_the_abi(lib):
+    cfg = _lib.CommConfig()
+    assert lib.nimbleCommConfigDefault(ctypes.byref(cfg)) == 0
+    assert (cfg.fabric, cfg.pipe_chunk, cfg.p2p_buffer, cfg.channels_per_peer) == (1, 64 << 10, 10 << 20, 1)
+    assert (cfg.ctas, cfg.direct_chunk, cfg.pull, cfg.push_chunk) == (0, 0, 0, 0)
+    assert cfg.nvlink_bytes_per_s == 900e9

@@ -285,6 +285,50 @@ def w_graph(comm, rank, R):
     return bads
 
 
+def w_overtake(comm, rank, R, big):
+    """Post slots are double-buffered by epoch parity.  A receiver that pulled
+    everything it needed from a sender does not wait for that sender, so it
+    can run two launches ahead and overwrite the post slot the sender has not
+    read yet.  The sender must infer the pull from the newer epoch instead of
+    waiting for a post that never comes back.  Here rank 1 is held in launch A
+    by a `big` self copy whose items surround its small segment for rank 0.
+    Rank 0 pulls that segment, runs launch B (its own self copy only), and
+    then launch C, whose post for rank 1 lands in A's slot."""
+    from paper_2604_00317_b200 import comm as C
+    comm.set_config(pull=2)  # every registered sender grants pulls
+    small = 4096 + 3
+
+    def mat(a10, a11, a00):
+        m = [0] * (R * R)
+        m[1 * R + 0], m[1 * R + 1], m[0] = a10, a11, a00
+        return m
+
+    mats = [mat(small, big, 0), mat(0, 0, 4096), mat(small, 0, 0)]
+    bufs, handles = [], []
+    for i, m in enumerate(mats):
+        sc, sd, rc, rd = C.packed_displs(m, R, rank)
+        send = torch.empty(max(sum(sc), 16), dtype=torch.uint8, device="cuda")
+        recv = torch.zeros(max(sum(rc), 16), dtype=torch.uint8, device="cuda")
+        for d in range(R):
+            C.fill_payload(send[sd[d]:], 0, sc[d], 40 + i, rank, d)
+        handles += [comm.register(send), comm.register(recv)]
+        bufs.append((m, sc, sd, recv, rc, rd, send))
+    torch.cuda.synchronize()
+    for m, sc, sd, recv, rc, rd, send in bufs:  # no host sync between the launches
+        comm.alltoallv(send, sc, sd, recv, rc, rd)
+    torch.cuda.synchronize()
+    comm.check_async()
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for i, (m, sc, sd, recv, rc, rd, send) in enumerate(bufs):
+        for s in range(R):
+            C.check_payload(recv[rd[s]:], 0, rc[s], 40 + i, s, rank, bad)
+    torch.cuda.synchronize()
+    for h in handles:
+        comm.deregister(h)
+    comm.set_config(pull=0)
+    return int(bad.item())
+
+
 def w_bench(comm, rank, R):
     return comm.bench_skewed(32 * MiB, 0.7, 0, warmup=1, iters=3)
 
@@ -355,7 +399,7 @@ def test_moe_dispatch_combine():
     R = min(_ngpus(), 4)
     res = _spawn("w_moe", R)
     assert all(ok for ok, _ in res.values()), res
-    assert res[0][1] > max(n for _, n in list(res.values())[1:])  # rank 0 holds the hot expert
+    assert res[0][1] > max(n for r, (_, n) in res.items() if r != 0)  # rank 0 holds the hot expert
 
 
 @need2
@@ -417,3 +461,9 @@ def test_comm_init_all_single_process_grouped():
         for c in comms:
             with torch.cuda.device(c.device):
                 c.destroy()
+
+
+@need2
+def test_receiver_two_launches_ahead_of_sender():
+    out = _spawn("w_overtake", 2, 4 << 30)
+    assert all(v == 0 for v in out.values()), out

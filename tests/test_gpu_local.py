@@ -175,6 +175,7 @@ def test_comm_config_validation():
     try:
         cfg = c.config()
         assert cfg.fabric == 1 and cfg.pipe_chunk == 64 << 10 and cfg.p2p_buffer == 10 << 20 and cfg.pull == 0
+        assert cfg.push_chunk == 0 and cfg.direct_chunk == 0
         with pytest.raises(NimbleError):
             c.set_config(fabric="alltoall", gpus_per_node=4)      # mesh model needs one GPU per rank
         with pytest.raises(NimbleError):

@@ -27,10 +27,10 @@ def _contiguous(ranges, start, total):
     assert pos == start + total
 
 
-def _check(topo, R, m, pipe_chunk=64 * KiB, dchunk=64 * KiB, staged=0, pull=0):
+def _check(topo, R, m, pipe_chunk=64 * KiB, dchunk=64 * KiB, staged=0, pull=0, pchunk=0):
     plan = P.plan(topo, R, R, m)
     sched = {r: P.debug_schedule(topo, R, R, m, r, pipe_chunk=pipe_chunk, direct_chunk=dchunk,
-                                 staged_mask=staged, pull_mask=pull) for r in range(R)}
+                                 staged_mask=staged, pull_mask=pull, push_chunk=pchunk) for r in range(R)}
     for pp in plan.pairs:
         s, d = pp.src, pp.dst
         off = 0
@@ -39,12 +39,13 @@ def _check(topo, R, m, pipe_chunk=64 * KiB, dchunk=64 * KiB, staged=0, pull=0):
             nbytes = int(nbytes)
             if c.cls == "direct":
                 push = [it for it in sched[s] if it["kind"] == "push" and it["peer"] == d]
-                assert all(it["bytes"] <= dchunk for it in push)
+                assert all(it["bytes"] <= (pchunk or dchunk) for it in push)
                 _contiguous(_ranges(push), off, nbytes)
                 assert [it["seq"] for it in push] == list(range(len(push)))
                 if (pull >> s) & 1:
                     pl = [it for it in sched[d] if it["kind"] == "pull" and it["peer"] == s]
                     _contiguous(_ranges(pl), off, nbytes)
+                    assert all(it["bytes"] <= dchunk for it in pl)
                 if (staged >> s) & 1:  # drained through d's self ring, same chunking
                     fw = [it for it in sched[d] if it["kind"] == "forward" and it["aux"] == s and it["peer"] == d]
                     assert [(it["dst"], it["bytes"], it["seq"]) for it in fw] == \
@@ -70,10 +71,11 @@ def test_nvswitch_skewed_direct_only(lib):
     assert all(it["kind"] == "push" for r in sched for it in sched[r])
 
 
+@pytest.mark.parametrize("pchunk", [0, 8 * KiB])
 @pytest.mark.parametrize("staged,pull", [(0, 0), (0b1111, 0), (0, 0b1111), (0b0101, 0b1010)])
-def test_receive_modes(lib, staged, pull):
+def test_receive_modes(lib, staged, pull, pchunk):
     t = P.build_canonical(1, 4, 0, 900e9, 0, P.NVSWITCH)
-    _check(t, 4, P.gen_irregular(4, 40 * MiB + 77, 0.8, 3), staged=staged, pull=pull)
+    _check(t, 4, P.gen_irregular(4, 40 * MiB + 77, 0.8, 3), staged=staged, pull=pull, pchunk=pchunk)
 
 
 def test_mesh_relays_p2p_1gib(lib):  # c2: 0 -> 1 over direct + via 2 + via 3

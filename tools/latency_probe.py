@@ -21,10 +21,13 @@ def main():
     dist.broadcast_object_list(uid, 0)
     comm = C.Comm.init_rank(world, uid[0], rank)
     R = world
-    for pull in (1, 2):
-        comm.set_config(pull=pull)
-        for mib in (1, 16, 256):
-            m = P.gen_skewed_a2av(R, mib * MiB, 0.7, 0)
+    pulls = [int(v) for v in os.environ.get("LAT_PULL", "1,2").split(",")]
+    chunks = [int(v) for v in os.environ.get("LAT_CHUNKS", "0").split(",")]
+    sizes = [int(v) for v in os.environ.get("LAT_KIB", "1024,16384,262144").split(",")]
+    for pull, chunk in [(p, c) for p in pulls for c in chunks]:
+        comm.set_config(pull=pull, direct_chunk=chunk)
+        for kib in sizes:
+            m = P.gen_skewed_a2av(R, kib * 1024, 0.7, 0)
             sc, sd, rc, rd = C.packed_displs(m, R, rank)
             send = torch.empty(max(sum(sc), 16), dtype=torch.uint8, device="cuda")
             recv = torch.empty(max(sum(rc), 16), dtype=torch.uint8, device="cuda")
@@ -49,7 +52,7 @@ def main():
             comm.check_async()
             if rank == 0:
                 bound = max(sum(m[s * R + v] for s in range(R) if s != v) for v in range(R)) / 900e9
-                print(f"pull={pull} {mib:4d}MiB: device {t[0]*1e6:8.1f}us/call  host {t[1]*1e6:6.1f}us/call "
+                print(f"pull={pull} chunk={chunk:6d} {kib:7d}KiB: device {t[0]*1e6:8.1f}us/call  host {t[1]*1e6:6.1f}us/call "
                       f"bound {bound*1e6:7.1f}us frac {bound/t[0]:.3f}", flush=True)
             comm.deregister(hs)
             comm.deregister(hr)

@@ -35,7 +35,7 @@ def port_bound(m, R):
                for v in range(R)) / 900e9
 
 
-def run_point(comm, pg, rank, R, m, name, fabric="nvswitch", iters=10, warmup=3, nccl=True, extra=None):
+def _run_point(comm, pg, rank, R, m, name, fabric="nvswitch", iters=10, warmup=3, nccl=True, extra=None):
     comm.set_config(fabric=fabric, gpus_per_node=R)
     sc, sd, rc, rd = C.packed_displs(m, R, rank)
     send = torch.empty(max(sum(sc), 16), dtype=torch.uint8, device="cuda")
@@ -106,9 +106,23 @@ def main():
     comm = C.Comm.init_rank(world, uid[0], rank)
     if os.environ.get("SWEEP_PULL"):
         comm.set_config(pull=int(os.environ["SWEEP_PULL"]))
+    for chunk in [int(v) for v in os.environ.get("SWEEP_CHUNKS", "0").split(",")]:
+        comm.set_config(direct_chunk=chunk)
+        sweep(comm, pg, rank, world, chunk)
+    dist.barrier()
+    comm.destroy()
+    dist.destroy_process_group()
+
+
+def sweep(comm, pg, rank, world, chunk):
     R = world
     cases = os.environ.get("SWEEP_CASES", "c3,c5,c4,c1,c2").split(",")
     per_rank = int(os.environ.get("SWEEP_PER_RANK_MIB", "256")) * MiB
+    nccl = os.environ.get("SWEEP_NCCL", "1") == "1"
+    tag = {"direct_chunk": chunk} if chunk else {}
+
+    def run_point(*a, extra=None, **k):
+        return _run_point(*a, nccl=nccl, extra=dict(extra or {}, **tag), **k)
     if "c3" in cases:
         for i in range(10):
             run_point(comm, pg, rank, R, P.gen_skewed_a2av(R, per_rank, i / 10, 0), "c3",
@@ -130,9 +144,6 @@ def main():
     if "c2" in cases and R == 4:
         for fab in ("nvswitch", "alltoall"):
             run_point(comm, pg, rank, R, P.gen_p2p(R, 0, 1, 1 << 30), "c2", fab, iters=5)
-    dist.barrier()
-    comm.destroy()
-    dist.destroy_process_group()
 
 
 if __name__ == "__main__":

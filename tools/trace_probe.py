@@ -10,7 +10,7 @@ from paper_2604_00317_b200 import comm as C  # noqa: E402
 from paper_2604_00317_b200 import planner as P  # noqa: E402
 
 MiB = 1 << 20
-NAMES = ["start", "prolog", "first", "last", "ctas", "signal", "waited"]
+NAMES = ["start", "prolog", "first", "last", "ctas", "signal", "waited", "cta0done"]
 
 
 def main():
@@ -25,7 +25,7 @@ def main():
     case = os.environ.get("TRACE_CASE", "skew")
     if case == "relay":
         comm.set_config(fabric="alltoall", gpus_per_node=R)
-    for pull in (1, 2):
+    for pull in [int(v) for v in os.environ.get("TRACE_PULL", "1,2").split(",")]:
         comm.set_config(pull=pull)
         for mib in ((64, 1024) if case == "relay" else (1, 256)):
             m = P.gen_p2p(R, 0, 1, mib * MiB) if case == "relay" else P.gen_skewed_a2av(R, mib * MiB, 0.7, 0)
@@ -42,7 +42,7 @@ def main():
                 t0 = min(t[0] for t in allt)
                 print(f"pull={pull} {mib}MiB (us from earliest kernel start; globaltimers assumed aligned)")
                 for r, t in enumerate(allt):
-                    print(f"  rank {r}: " + " ".join(f"{n}={(v - t0) / 1e3:8.1f}" for n, v in zip(NAMES, t[:7])),
+                    print(f"  rank {r}: " + " ".join(f"{n}={(v - t0) / 1e3:8.1f}" for n, v in zip(NAMES, t[:8])),
                           flush=True)
             comm.deregister(hs)
             comm.deregister(hr)
