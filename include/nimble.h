@@ -194,8 +194,9 @@ typedef struct {
                                      pipe_chunk)                                           */
     int pull;                     /* receiver-driven pulls.  0 = auto (default): receivers
                                      ask; a registered sender grants unless its own port is
-                                     ingress-bound (ingress > 1.55 x egress), in which case it
-                                     pushes out; 1 = never (push only); 2 = always grant */
+                                     ingress-bound (ingress > 1.2 x egress; 1.55 x with two
+                                     ranks), in which case it pushes out; 1 = never (push
+                                     only); 2 = always grant                             */
     uint64_t push_chunk;          /* work-item size of direct pushes (<= pipe_chunk), 0 = auto
                                      (8 KiB).  A port that pulls in while it pushes out runs
                                      both through one CTA ring; short pushes keep a store

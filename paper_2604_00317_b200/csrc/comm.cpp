@@ -487,11 +487,17 @@ void fill_posts(nimbleComm* c, RankBuffers& rb, const PlanResult& plan) {
     //  - pull responses carry 16 B of protocol per 128 B, writes 24 B;
     //  - mixing pushes and pulls on links busy both ways is slow.
     // Receivers always ask to pull; a sender declines -- and pushes its data
-    // out -- only when its own port is clearly ingress-bound (ingress > 1.55 x
-    // egress: the crossover measured on 2 and 3 GPUs), so the hot port of a
-    // skewed exchange pulls everything in and pushes everything out.
+    // out -- only when its own port is clearly ingress-bound, so the hot port
+    // of a skewed exchange pulls everything in and pushes everything out.
+    // "Clearly": ingress > 1.2 x egress with three or more ranks, > 1.55 x with
+    // two.  A decliner drives both directions from its own engine (~1.08 TB/s
+    // of pushes plus pulls on one B200) while its peers' engines lose that
+    // work; with a single peer nothing else is left for the peer to do, so
+    // declining pays only at a larger imbalance (profiles/r01_pull_policy.md,
+    // threshold study on 2-4 GPUs with 8 KiB pushes).
     rb.pull = c->cfg.pull != 1;
-    const bool grant = c->cfg.pull == 2 || (c->cfg.pull == 0 && ingress * 20 <= egress * 31);
+    const uint64_t num = rb.R == 2 ? 31 : 6, den = rb.R == 2 ? 20 : 5;
+    const bool grant = c->cfg.pull == 2 || (c->cfg.pull == 0 && ingress * den <= egress * num);
     rb.send_post.assign(static_cast<size_t>(rb.R), Post{});
     for (int d = 0; d < rb.R; ++d) {
         if (d == rb.me || rb.send_bytes[d] == 0) continue;
