@@ -495,9 +495,15 @@ void fill_posts(nimbleComm* c, RankBuffers& rb, const PlanResult& plan) {
     // work; with a single peer nothing else is left for the peer to do, so
     // declining pays only at a larger imbalance (profiles/r01_pull_policy.md,
     // threshold study on 2-4 GPUs with 8 KiB pushes).
-    rb.pull = c->cfg.pull != 1;
+    // Two ranks whose directions are within 1.5x of each other both push: with
+    // every byte crossing the one link pair in both directions, pull requests
+    // ride on the other direction's data and two-way pushes come out ahead
+    // (0.75 vs 0.72-0.74 of the bound at r >= 0.7 and for uniform traffic).
+    // Each rank's row and column are the whole 2x2 matrix, so both decide alike.
+    const bool two_way_push = c->cfg.pull == 0 && rb.R == 2 && ingress * 2 <= egress * 3 && egress * 2 <= ingress * 3;
+    rb.pull = c->cfg.pull != 1 && !two_way_push;
     const uint64_t num = rb.R == 2 ? 31 : 6, den = rb.R == 2 ? 20 : 5;
-    const bool grant = c->cfg.pull == 2 || (c->cfg.pull == 0 && ingress * den <= egress * num);
+    const bool grant = c->cfg.pull == 2 || (c->cfg.pull == 0 && !two_way_push && ingress * den <= egress * num);
     rb.send_post.assign(static_cast<size_t>(rb.R), Post{});
     for (int d = 0; d < rb.R; ++d) {
         if (d == rb.me || rb.send_bytes[d] == 0) continue;
