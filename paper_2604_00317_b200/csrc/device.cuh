@@ -1,7 +1,7 @@
 // Plain-old-data shared by the host runtime and the sm_100a forwarding engine.
 //
 // Per rank the comm owns two IPC-exported device regions:
-//   ctrl    : Ctrl header (receive posts + done flags) followed by the ready
+//   ctrl    : Ctrl header (posts, done / pulled counters) followed by the ready
 //             flags of the staging rings hosted here and the consumed flags of
 //             the rings this rank feeds;
 //   staging : one ring of `slots` x `pipe_chunk` bytes per ordered pair (s,d)
@@ -75,8 +75,9 @@ static_assert(sizeof(Post) == 32, "Post layout");
 // a reader accepts it once all three words carry its epoch:
 //   w[0] = epoch32 << 32 | win << 16 | mode,  w[1] = epoch16 << 48 | off,
 //   w[2] = epoch16 << 48 | bytes            (off, bytes < 2^48).
-// Double-buffered by epoch parity: epoch e's post stays intact until every
-// peer has finished epoch e (no rank can reach e + 2 before that).
+// Double-buffered by epoch parity.  A writer that never has to wait for a
+// reader can reach epoch e + 2 and overwrite the slot first; the reader then
+// sees a newer epoch and infers the outcome (engine.cu, read_post).
 struct WirePost {
     uint64_t w[4];
 };
@@ -89,9 +90,9 @@ struct WirePost {
 // epoch e without needing the reader (see read_post in engine.cu).
 struct CtrlHeader {
     WirePost post[2][kMaxRanks];       // written by me (the receiver), read by relays
-    uint64_t done[kMaxRanks];          // done[w] = epoch: writer w finished writing into me
+    uint64_t done[kMaxRanks];          // done[w] >= epoch << 32: writer w finished writing into me
     WirePost send_post[2][kMaxRanks];  // send_post[e][s]: pushed by sender s, read by me
-    uint64_t pulled[kMaxRanks];        // pulled[d] = epoch: receiver d finished pulling from me
+    uint64_t pulled[kMaxRanks];        // pulled[d] >= epoch << 32: receiver d finished pulling from me
     WirePost post_in[2][kMaxRanks];    // post_in[e][d]: pushed by receiver d, read by me
 };
 

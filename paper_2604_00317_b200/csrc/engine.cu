@@ -69,6 +69,10 @@ __device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
     asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ void red_add_sys(uint64_t* p, uint64_t v) {
+    asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ uint64_t global_ns() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -365,7 +369,7 @@ __device__ Prep prepare(SharedState& sh, const LaunchArgs& a, const Item& it, ui
         const int s = it.peer;
         if (!resolve_send(sh, a, s)) return kSkip;
         if (sh.send_mode[s] != kSendRegistered) return kSkip;  // declined: s pushes instead
-        src = sh.send_base[s] + it.src;  // pulled[] is raised once per launch (epilogue)
+        src = sh.send_base[s] + it.src;  // pulled[] is counted once per CTA (epilogue)
         return kGo;
     }
     if (it.kind == kPush || it.kind == kStage) {
@@ -375,7 +379,7 @@ __device__ Prep prepare(SharedState& sh, const LaunchArgs& a, const Item& it, ui
             if (!resolve(sh, a, d, me)) return kSkip;
             if (pull_granted_to(sh, a, d)) return kSkip;  // d pulls this range itself
             if ((sh.seg_mode[d * kMaxRanks + me] & 0xf) == kPostZeroCopy) {
-                dst = sh.seg_base[d * kMaxRanks + me] + it.dst;  // done[] is raised once per launch
+                dst = sh.seg_base[d * kMaxRanks + me] + it.dst;  // done[] is counted once per CTA (epilogue)
                 return kGo;
             }
         }
@@ -660,29 +664,44 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
     }
     __syncthreads();
 
-    // Epilogue: the last CTA out publishes this rank's completions and waits
-    // for everyone else's -- one warp, lane p handling peer p, so the remote
-    // reads and waits run in parallel.  Then it resets the per-launch scratch
-    // for the next stream-ordered launch.
+    // Epilogue.  done[me] / pulled[me] at every peer are per-pair counters that
+    // gain exactly 2^32 per launch, so "epoch e complete" is counter >= e << 32:
+    // each CTA, once its own writes are fenced, adds 1 for every peer it may
+    // have written into (done) or pulled from (pulled); the last CTA adds the
+    // rest (2^32 - grid, or 2^32 for a peer this launch does not touch).  The
+    // sum can only reach the threshold after every CTA's add has landed, and
+    // every add is issued after that CTA's fence -- so the last CTA needs no
+    // second system fence.  It then waits for everyone else's completions --
+    // one warp, lane p handling peer p -- and resets the per-launch scratch for
+    // the next stream-ordered launch.
     __shared__ uint32_t last_cta;
-    if (tid == 0) {
-        // this CTA's peer writes before the rank-wide completion count (pulls
-        // and local copies only read remote memory: a GPU-scope fence will do)
-        if (sh.remote_writes) __threadfence_system();
-        else __threadfence();
-        trace_min(a, kTraceFirstCtaDone);
-        last_cta = atomicAdd(&scratch[1], 1u) + 1 == gridDim.x;
+    if (tid < 32) {
+        if (tid == 0) {
+            // this CTA's peer writes before its completion adds (pulls and local
+            // copies only read remote memory: a GPU-scope fence will do)
+            if (sh.remote_writes) __threadfence_system();
+            else __threadfence();
+            trace_min(a, kTraceFirstCtaDone);
+        }
+        __syncwarp();
+        if (!a.local_only && tid < R) {
+            CtrlHeader* ph = reinterpret_cast<CtrlHeader*>(c->ctrl[tid]);
+            if ((a.write_targets >> tid) & 1) red_add_sys(&ph->done[me], 1);
+            if ((a.pull_req >> tid) & 1) red_add_sys(&ph->pulled[me], 1);
+        }
+        __syncwarp();
+        if (tid == 0) last_cta = atomicAdd(&scratch[1], 1u) + 1 == gridDim.x;
     }
     __syncthreads();
     if (last_cta && tid < 32) {
         const int lane = tid;
         if (lane == 0) trace_max(a, kTraceCtasDone);
         if (!a.local_only) {
-            asm volatile("fence.acq_rel.sys;" ::: "memory");  // warp-wide: all CTAs' writes -> flags
+            const uint64_t full = 1ull << 32, done_tag = a.epoch << 32;
             if (lane < R) {
                 CtrlHeader* ph = reinterpret_cast<CtrlHeader*>(c->ctrl[lane]);
-                if ((a.write_targets >> lane) & 1) st_relaxed(&ph->done[me], a.epoch);
-                if ((a.pull_req >> lane) & 1) st_relaxed(&ph->pulled[me], a.epoch);
+                red_add_sys(&ph->done[me], ((a.write_targets >> lane) & 1) ? full - gridDim.x : full);
+                red_add_sys(&ph->pulled[me], ((a.pull_req >> lane) & 1) ? full - gridDim.x : full);
             }
             __syncwarp();
             if (lane == 0) trace_max(a, kTraceSignalled);
@@ -696,9 +715,9 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
                 bool need_done = (a.relay_writers >> w) & 1;
                 if (((a.recv_direct >> w) & 1) && ((a.recv_zc >> w) & 1))  // w pushed in place unless I pulled
                     need_done |= !(((a.pull_req >> w) & 1) && decide[kMaxRanks + w] == kDecidePull);
-                if (need_done) wait_ge(&h->done[w], a.epoch, c, kErrDoneTimeout);
+                if (need_done) wait_ge(&h->done[w], done_tag, c, kErrDoneTimeout);
                 if (((a.push_targets >> w) & 1) && decide[w] == kDecidePull)  // w pulled my segment
-                    wait_ge(&h->pulled[w], a.epoch, c, kErrDoneTimeout);
+                    wait_ge(&h->pulled[w], done_tag, c, kErrDoneTimeout);
             }
             __syncwarp();
         }
