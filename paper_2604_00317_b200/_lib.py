@@ -39,7 +39,7 @@ class CommConfig(ctypes.Structure):  # nimbleCommConfig
     _fields_ = [("fabric", c_int), ("gpus_per_node", c_int), ("nvlink_bytes_per_s", c_double),
                 ("planner", PlannerConfig), ("pipe_chunk", c_u64), ("p2p_buffer", c_u64),
                 ("channels_per_peer", c_int), ("ctas", c_int), ("direct_chunk", c_u64), ("pull", c_int),
-                ("push_chunk", c_u64)]
+                ("push_chunk", c_u64), ("ll_max", c_u64)]
 
 
 class UniqueId(ctypes.Structure):  # nimbleUniqueId

@@ -19,18 +19,29 @@ def _ptr(t) -> int:
     return t.data_ptr() if hasattr(t, "data_ptr") else int(t)
 
 
+def _current_stream() -> int:
+    import torch
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)  # no Stream object per call
+    if raw is not None:
+        return raw(torch.cuda.current_device())
+    return torch.cuda.current_stream().cuda_stream
+
+
 def _stream_handle(stream) -> int:
     if stream is None:
-        import torch
-        return torch.cuda.current_stream().cuda_stream
+        return _current_stream()
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
+_SIZE_ARRAYS: dict = {}
+
+
 def _sizes(values):
-    arr = (c_size * len(values))()
-    for i, v in enumerate(values):
-        arr[i] = int(v)
-    return arr
+    n = len(values)
+    t = _SIZE_ARRAYS.get(n)
+    if t is None:
+        t = _SIZE_ARRAYS[n] = c_size * n
+    return t(*values)
 
 
 def unique_id() -> bytes:
@@ -123,9 +134,9 @@ class Comm:
 
     # -- data path (counts / displacements in bytes: uint8 datatype)
     def alltoallv(self, send, sendcounts, sdispls, recv, recvcounts, rdispls, stream=None, datatype=UINT8):
-        _lib.call("nimbleAlltoAllv", c_void_p(_ptr(send)), _sizes(sendcounts), _sizes(sdispls),
-                  c_void_p(_ptr(recv)), _sizes(recvcounts), _sizes(rdispls), datatype, self._h,
-                  c_void_p(_stream_handle(stream)))
+        fn = _lib.lib().nimbleAlltoAllv  # argtypes convert plain ints to pointers
+        _lib.check(fn(_ptr(send), _sizes(sendcounts), _sizes(sdispls), _ptr(recv), _sizes(recvcounts),
+                      _sizes(rdispls), datatype, self._h, _stream_handle(stream)))
 
     def alltoall(self, send, recv, count, stream=None, datatype=UINT8):
         _lib.call("nimbleAlltoAll", c_void_p(_ptr(send)), c_void_p(_ptr(recv)), count, datatype, self._h,

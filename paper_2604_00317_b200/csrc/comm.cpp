@@ -171,6 +171,7 @@ struct CachedSchedule {
     DevBuf<Post> posts;
     DevBuf<Post> send_posts;
     DevBuf<uint64_t> finals;
+    DevBuf<Item> ll_items;
 };
 
 struct Clique;
@@ -236,6 +237,16 @@ struct nimbleComm {
     uint64_t plan_ids = 0;
     std::list<nb::CachedPlan> plans;
     std::list<nb::CachedSchedule> schedules;
+    // Repeat fast path: the previous stand-alone all-to-allv (buffers, counts;
+    // nvswitch model) and the cached schedule it launched.  Cleared whenever
+    // schedules, windows or the config change.
+    struct {
+        nb::CachedSchedule* cs = nullptr;
+        nb::RankBuffers rb;
+        uint64_t key[2 + 4 * nb::kMaxRanks];
+    } fast;
+    nb::CachedSchedule* last_cs = nullptr;  // schedule of the most recent launch
+    nb::RankBuffers last_rb;
     cudaStream_t bench_stream = nullptr;
     uint64_t* d_trace = nullptr;  // NIMBLE_TRACE=1: device timeline of the last launch
     cudaEvent_t last_launch = nullptr;  // launches on one comm are serialized across streams
@@ -303,6 +314,7 @@ void default_config(nimbleCommConfig* cfg, int nranks) {
     cfg->direct_chunk = 0;
     cfg->pull = 0;
     cfg->push_chunk = 0;
+    cfg->ll_max = kLLMaxData;
 }
 
 // Allocate ctrl + staging, exchange handles / pointers, map peers.
@@ -505,8 +517,9 @@ void fill_posts(nimbleComm* c, RankBuffers& rb, const PlanResult& plan) {
     const uint64_t num = rb.R == 2 ? 31 : 6, den = rb.R == 2 ? 20 : 5;
     const bool grant = c->cfg.pull == 2 || (c->cfg.pull == 0 && !two_way_push && ingress * den <= egress * num);
     rb.send_post.assign(static_cast<size_t>(rb.R), Post{});
+    const uint64_t ll_max = c->cfg.ll_max;
     for (int d = 0; d < rb.R; ++d) {
-        if (d == rb.me || rb.send_bytes[d] == 0) continue;
+        if (d == rb.me || rb.send_bytes[d] == 0 || ll_pair(plan, rb.me, d, rb.send_bytes[d], ll_max)) continue;
         Post p{};
         p.tag = 1;
         p.bytes = rb.send_bytes[d];
@@ -527,7 +540,7 @@ void fill_posts(nimbleComm* c, RankBuffers& rb, const PlanResult& plan) {
             for (const Flow& f : pr.flows) relayed[static_cast<size_t>(pr.src)] |= pr.cands[static_cast<size_t>(f.cand)].via >= 0;
     rb.recv_post.assign(static_cast<size_t>(rb.R), Post{});
     for (int s = 0; s < rb.R; ++s) {
-        if (s == rb.me || rb.recv_bytes[s] == 0) continue;
+        if (s == rb.me || rb.recv_bytes[s] == 0 || ll_pair(plan, s, rb.me, rb.recv_bytes[s], ll_max)) continue;
         Post p{};
         p.tag = 1;
         p.bytes = rb.recv_bytes[s];
@@ -547,7 +560,8 @@ void fill_posts(nimbleComm* c, RankBuffers& rb, const PlanResult& plan) {
 CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& plan, const RankBuffers& rb,
                              cudaStream_t st) {
     std::vector<uint64_t> key = {plan_id, c->cfg.pipe_chunk, c->cfg.p2p_buffer,
-                                 static_cast<uint64_t>(c->cfg.channels_per_peer), c->cfg.direct_chunk, c->cfg.push_chunk};
+                                 static_cast<uint64_t>(c->cfg.channels_per_peer), c->cfg.direct_chunk, c->cfg.push_chunk,
+                                 c->cfg.ll_max};
     for (int r = 0; r < rb.R; ++r) {
         key.push_back(rb.send_ptr[r]);
         key.push_back(rb.send_bytes[r]);
@@ -568,6 +582,7 @@ CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& 
     if (cap != cudaStreamCaptureStatusNone)
         throw Error(nimbleInvalidUsage, "graph capture: run the same exchange once before capturing it "
                                         "(its schedule must be cached; capture does not allow uploads)");
+    c->fast.cs = nullptr;  // entries may be recycled below
     CachedSchedule cs;
     cs.key = key;
     const char* env = std::getenv("NIMBLE_DIRECT_CHUNK");
@@ -575,7 +590,7 @@ CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& 
                             : env && *env          ? std::strtoull(env, nullptr, 0)
                                                    : kDefaultDirectChunk;
     cs.sc = build_schedule(plan, rb, c->cfg.pipe_chunk, slot_count(c->cfg), dchunk,
-                           c->cfg.push_chunk ? c->cfg.push_chunk : kDefaultPushChunk);
+                           c->cfg.push_chunk ? c->cfg.push_chunk : kDefaultPushChunk, c->cfg.ll_max);
     if (c->schedules.size() >= 4) {  // recycle the oldest entry's device buffers
         CUDA_TRY(cudaDeviceSynchronize());  // no launch may still read them
         CachedSchedule& old = c->schedules.back();
@@ -583,12 +598,14 @@ CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& 
         cs.posts = std::move(old.posts);
         cs.send_posts = std::move(old.send_posts);
         cs.finals = std::move(old.finals);
+        cs.ll_items = std::move(old.ll_items);
         c->schedules.pop_back();
     }
     cs.items.assign(cs.sc.items, st);
     cs.posts.assign(cs.sc.posts, st);
     cs.send_posts.assign(cs.sc.send_posts, st);
     cs.finals.assign(cs.sc.final_waits, st);
+    cs.ll_items.assign(cs.sc.ll_items, st);
     c->schedules.push_front(std::move(cs));
     return c->schedules.front();
 }
@@ -614,6 +631,10 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     a.write_targets = cs.sc.write_targets;
     a.final_waits = cs.finals.p;
     a.nfinal = static_cast<uint32_t>(cs.sc.final_waits.size() / 2);
+    a.n_ll_send = cs.sc.n_ll_send;
+    a.n_ll_recv = cs.sc.n_ll_recv;
+    a.ll_items = cs.ll_items.p;
+    a.ll_senders = cs.sc.ll_senders;
     a.local_only = 0;
     if (c->d_trace) {
         static const uint64_t init[kTraceSlots] = {~0ull, 0, ~0ull, 0, 0, 0, 0, ~0ull};
@@ -622,7 +643,8 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     }
     int ctas = c->cfg.ctas > 0 ? c->cfg.ctas : c->sms;
     // small exchanges: no more CTAs than items (each CTA costs a fence at exit)
-    ctas = std::max(1, std::min({ctas, c->sms, static_cast<int>(std::max<size_t>(cs.sc.items.size(), 1))}));
+    const size_t work = cs.sc.items.size() + cs.sc.ll_items.size();
+    ctas = std::max(1, std::min({ctas, c->sms, static_cast<int>(std::max<size_t>(work, 1))}));
     // every rank launches even with nothing to move: its posts and done
     // flags are what its peers wait for.  Launches of one comm share its
     // scratch and flags, so a launch on another stream waits for the last one.
@@ -693,6 +715,8 @@ void run_exchanges(std::vector<Exchange>& exs) {
             evs.push_back(e);
         }
         launch(c, cs, ex.rb, ex.stream);
+        c->last_cs = &cs;
+        c->last_rb = ex.rb;
         for (size_t i = 0; i < ex.others.size(); ++i) {
             CUDA_TRY(cudaEventRecord(evs[i], ex.stream));
             CUDA_TRY(cudaStreamWaitEvent(ex.others[i], evs[i], 0));
@@ -775,6 +799,7 @@ void* register_window(nimbleComm* c, void* buff, size_t size) {
         }
     }
     c->windows.push_back(std::move(w));
+    c->fast.cs = nullptr;  // new window: posts of the same buffers may change
     c->view.nwin = static_cast<uint32_t>(c->windows.size());
     return reinterpret_cast<void*>(static_cast<uintptr_t>(id) + 1);
 }
@@ -815,6 +840,7 @@ void bench_matrix(nimbleComm* c, const std::vector<uint64_t>& m, int warmup, int
                 c->windows[k].opened.clear();
             }
             c->schedules.clear();
+            c->fast.cs = c->last_cs = nullptr;
             for (void* b : bufs) cudaFree(b);
         }
     } scope{c, {}, c->windows.size()};
@@ -986,6 +1012,7 @@ nimbleResult_t nimbleCommDestroy(nimbleComm_t c) {
             for (nb::Window& w : c->windows)
                 for (void* p : w.opened) nb::ipc_cache().release(p);
             c->schedules.clear();
+            c->fast.cs = c->last_cs = nullptr;
             nb::free_regions(c);
             cudaFree(c->d_view);
             cudaFree(c->d_win_table);
@@ -1031,8 +1058,10 @@ nimbleResult_t nimbleCommGetAsyncError(nimbleComm_t c, nimbleResult_t* err) {
                                      "timeout waiting for a relayed chunk", "timeout waiting for a writer's done flag",
                                      "send and receive counts disagree across ranks",
                                      "relay routes need a registered receive buffer",
-                                     "timeout waiting for a relay to drain"};
-        nb::g_last_error = code < 8 ? what[code] : "unknown device error";
+                                     "timeout waiting for a relay to drain",
+                                     "a post was overwritten before it was read (protocol violation)",
+                                     "timeout on a low-latency (LL) slot"};
+        nb::g_last_error = code < sizeof what / sizeof what[0] ? what[code] : "unknown device error";
     }
     return nimbleSuccess;
 }
@@ -1047,6 +1076,8 @@ nimbleResult_t nimbleCommSetConfig(nimbleComm_t c, const nimbleCommConfig* cfg) 
         if (!(next.nvlink_bytes_per_s > 0)) throw nb::Error(nimbleInvalidArgument, "config: bandwidth must be positive");
         nb::slot_count(next);
         nb::to_params(&next.planner);
+        if (next.ll_max > nb::kLLMaxData)
+            throw nb::Error(nimbleInvalidArgument, "config: ll_max above the LL slot size (64 KiB)");
         const bool regrow = next.pipe_chunk != c->cfg.pipe_chunk || next.p2p_buffer != c->cfg.p2p_buffer ||
                             next.channels_per_peer != c->cfg.channels_per_peer;
         nb::DeviceGuard g(c->device);
@@ -1067,6 +1098,7 @@ nimbleResult_t nimbleCommSetConfig(nimbleComm_t c, const nimbleCommConfig* cfg) 
         c->cfg = next;
         c->plans.clear();
         c->schedules.clear();
+        c->fast.cs = c->last_cs = nullptr;
         if (c->boot) c->boot->barrier();
     });
 }
@@ -1097,6 +1129,7 @@ nimbleResult_t nimbleCommDeregister(const nimbleComm_t c, void* handle) {
         c->windows[id].opened.clear();
         c->windows[id].live = false;
         c->schedules.clear();
+        c->fast.cs = c->last_cs = nullptr;
     });
 }
 
@@ -1150,16 +1183,41 @@ nimbleResult_t nimbleAlltoAllv(const void* sendbuff, const size_t sendcounts[], 
         if (!comm || !sendcounts || !sdispls || !recvcounts || !rdispls)
             throw nb::Error(nimbleInvalidArgument, "alltoallv: null argument");
         const size_t es = nb::elem_size(dt);
+        const int R = comm->nranks;
+        // The same stand-alone call as last time (same buffers and counts, no
+        // group, nvswitch model: the plan needs only this rank's row and
+        // column) relaunches its cached schedule directly.
+        uint64_t key[2 + 4 * nb::kMaxRanks];
+        key[0] = reinterpret_cast<uint64_t>(sendbuff);
+        key[1] = reinterpret_cast<uint64_t>(recvbuff);
+        for (int p = 0; p < R; ++p) {
+            key[2 + 4 * p] = sendcounts[p] * es;
+            key[3 + 4 * p] = sdispls[p] * es;
+            key[4 + 4 * p] = recvcounts[p] * es;
+            key[5 + 4 * p] = rdispls[p] * es;
+        }
+        const size_t key_bytes = sizeof(uint64_t) * (2 + 4 * static_cast<size_t>(R));
+        const bool standalone = nb::g_group_depth == 0 && comm->cfg.fabric == nimbleFabricNvSwitch;
+        if (standalone && comm->fast.cs && std::memcmp(key, comm->fast.key, key_bytes) == 0) {
+            nb::DeviceGuard g(comm->device);
+            nb::launch(comm, *comm->fast.cs, comm->fast.rb, static_cast<cudaStream_t>(stream));
+            return;
+        }
         nb::PendingOp op{nb::PendingOp::AllToAllV, comm, static_cast<cudaStream_t>(stream), -1, 0, 0,
                          reinterpret_cast<uint64_t>(sendbuff), reinterpret_cast<uint64_t>(recvbuff), {}, {}, {}, {}};
-        for (int p = 0; p < comm->nranks; ++p) {
-            op.sbytes.push_back(sendcounts[p] * es);
-            op.soff.push_back(sdispls[p] * es);
-            op.rbytes.push_back(recvcounts[p] * es);
-            op.roff.push_back(rdispls[p] * es);
+        for (int p = 0; p < R; ++p) {
+            op.sbytes.push_back(key[2 + 4 * p]);
+            op.soff.push_back(key[3 + 4 * p]);
+            op.rbytes.push_back(key[4 + 4 * p]);
+            op.roff.push_back(key[5 + 4 * p]);
         }
         nimbleResult_t r = nb::enqueue(std::move(op));
         if (r != nimbleSuccess) throw nb::Error(r, nb::g_last_error);
+        if (standalone && comm->last_cs) {
+            std::memcpy(comm->fast.key, key, key_bytes);
+            comm->fast.cs = comm->last_cs;
+            comm->fast.rb = comm->last_rb;
+        }
     });
 }
 

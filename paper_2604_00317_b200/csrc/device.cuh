@@ -28,12 +28,24 @@ constexpr int kMaxRanks = 32;
 constexpr int kMaxSlots = 256;
 constexpr int kThreads = 512;  // forwarding-engine CTA size
 
+// Low-latency (LL) protocol for small direct pairs: the sender stores 16-byte
+// lines {data[0:4], flag, data[4:8], flag} (flag = epoch, low 32 bits) into a
+// per-sender slot inside the receiver's ctrl region, which the receiver polls
+// and decodes -- no posts, no fences, no completion handshake.  Line 0 carries
+// the byte count.  Slots are double-buffered by epoch parity; a sender reuses
+// slot e & 1 only after the receiver acknowledged epoch e - 2 (ll_ack).
+constexpr uint64_t kLLMaxData = 64ull << 10;                                // bytes per pair
+constexpr uint64_t kLLPiece = 8ull << 10;                                   // bytes per work item (one CTA)
+constexpr uint64_t kLLSlotBytes = ((1 + kLLMaxData / 8) * 16 + 255) / 256 * 256;  // header + lines
+
 enum ItemKind : uint8_t {
     kLocal = 0,    // src -> dst, both local absolute addresses
     kPush = 1,     // my send range -> receiver `peer` (zero copy, or its self ring when staged)
     kStage = 2,    // my send range -> ring (me, aux) hosted on relay `peer`
     kForward = 3,  // ring (aux, peer) hosted here -> receiver `peer` (or my own buffer)
     kPull = 4,     // sender `peer`'s registered send range -> my buffer (receiver-driven)
+    kLLSend = 5,   // my small segment -> LL slot at receiver `peer` (separate list, see LaunchArgs)
+    kLLRecv = 6,   // LL slot of sender `peer` -> my buffer
 };
 
 // One unit of the chunk schedule, 32 bytes.
@@ -94,6 +106,7 @@ struct CtrlHeader {
     WirePost send_post[2][kMaxRanks];  // send_post[e][s]: pushed by sender s, read by me
     uint64_t pulled[kMaxRanks];        // pulled[d] >= epoch << 32: receiver d finished pulling from me
     WirePost post_in[2][kMaxRanks];    // post_in[e][d]: pushed by receiver d, read by me
+    uint64_t ll_ack[kMaxRanks];        // ll_ack[d] = epoch: receiver d finished that launch (its LL slots drained)
 };
 
 // Geometry of the flag arrays that follow the header inside ctrl.
@@ -108,7 +121,12 @@ struct FlagLayout {
         return header + 8ull * static_cast<uint64_t>(R) * R * kMaxSlots +
                8ull * ((static_cast<uint64_t>(d) * R + v) * kMaxSlots + slot);
     }
-    __host__ __device__ static constexpr uint64_t bytes(int R) { return header + 16ull * R * R * kMaxSlots; }
+    __host__ __device__ static constexpr uint64_t flags_end(int R) { return header + 16ull * R * R * kMaxSlots; }
+    // LL slot of sender s hosted here, epoch parity e: [e][s]
+    __host__ __device__ static constexpr uint64_t ll_off(int R, int e, int s) {
+        return flags_end(R) + (static_cast<uint64_t>(e) * R + s) * kLLSlotBytes;
+    }
+    __host__ __device__ static constexpr uint64_t bytes(int R) { return ll_off(R, 2, 0); }
 };
 
 // Comm-lifetime device view (set up once at init / registration).
@@ -144,6 +162,10 @@ struct LaunchArgs {
     uint64_t send_bytes[kMaxRanks];   // my outgoing pair sizes (checked against receivers' posts)
     const uint64_t* final_waits;      // pairs (ctrl byte offset of consumed flag, chunk index)
     uint32_t nfinal;
+    uint32_t n_ll_send, n_ll_recv;    // LL items: ll_items[0, n_ll_send) sends, then receives
+    const Item* ll_items;             // pieces of <= kLLPiece: kLLSend src / kLLRecv dst absolute, peer = the
+                                      // other end, seq = piece index, pad = the pair's byte count
+    uint64_t ll_senders;              // senders whose LL slot I drain this launch
     uint32_t local_only;              // 1: flagless single-GPU exchange (no ctrl)
     uint64_t* trace;                  // optional globaltimer stamps (NIMBLE_TRACE=1), see kTrace*
 };

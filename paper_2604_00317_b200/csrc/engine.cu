@@ -135,6 +135,7 @@ enum AsyncCode : uint32_t {
     kErrRelayToStaged = 6,
     kErrFinalTimeout = 7,
     kErrPostLost = 8,  // a post was overwritten in a way the protocol does not allow
+    kErrLLTimeout = 9,   // an LL slot never filled (or its receiver never drained the previous one)
 };
 
 // Producer-thread wait until *p >= tag; false (and an async error) on timeout
@@ -429,6 +430,120 @@ __device__ __forceinline__ void trace_max(const LaunchArgs& a, int slot) {
     if (a.trace) atomicMax(reinterpret_cast<unsigned long long*>(a.trace + slot), global_ns());
 }
 
+// ---- low-latency (LL) protocol for small direct pairs (device.cuh, kLLMaxData) ----
+
+__device__ __forceinline__ void st_ll(uint4* p, uint32_t lo, uint32_t hi, uint32_t flag) {
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(lo), "r"(flag), "r"(hi),
+                 "r"(flag)
+                 : "memory");
+}
+
+__device__ __forceinline__ uint4 ld_ll(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+
+// Bytes [off, off + n) of p (n <= 8) as a little-endian word; any alignment.
+__device__ __forceinline__ uint64_t load_upto8(const uint8_t* p, uint32_t n) {
+    if (n == 8 && (reinterpret_cast<uintptr_t>(p) & 7) == 0) return *reinterpret_cast<const uint64_t*>(p);
+    uint64_t v = 0;
+    for (uint32_t i = 0; i < n; ++i) v |= static_cast<uint64_t>(p[i]) << (8 * i);
+    return v;
+}
+
+__device__ __forceinline__ void store_upto8(uint8_t* p, uint64_t v, uint32_t n) {
+    if (n == 8 && (reinterpret_cast<uintptr_t>(p) & 7) == 0) {
+        *reinterpret_cast<uint64_t*>(p) = v;
+        return;
+    }
+    for (uint32_t i = 0; i < n; ++i) p[i] = static_cast<uint8_t>(v >> (8 * i));
+}
+
+// Every CTA, all threads, at kernel start: my small segments straight into
+// the receivers' LL slots.  The only wait is for the slot's previous use
+// (epoch - 2) to have been drained, which is almost always long done.
+__device__ void ll_send_all(const LaunchArgs& a) {
+    const CommDevice* c = a.comm;
+    const int me = c->rank, R = c->nranks;
+    const uint32_t flag = static_cast<uint32_t>(a.epoch);
+    __shared__ uint32_t ok;
+    for (uint32_t j = blockIdx.x; j < a.n_ll_send; j += gridDim.x) {
+        const Item it = a.ll_items[j];
+        const int d = it.peer;
+        if (threadIdx.x == 0) {
+            const CtrlHeader* h = reinterpret_cast<const CtrlHeader*>(c->ctrl[me]);
+            ok = a.epoch <= 2 || wait_ge(&h->ll_ack[d], a.epoch - 2, c, kErrLLTimeout);
+        }
+        __syncthreads();
+        if (ok) {
+            // line 0: the pair's byte count (written by piece 0); piece p's data
+            // byte b sits in line 1 + (p * kLLPiece + b) / 8
+            uint4* slot = reinterpret_cast<uint4*>(c->ctrl[d] + FlagLayout::ll_off(R, static_cast<int>(a.epoch & 1), me));
+            uint4* lines0 = slot + 1 + it.seq * (kLLPiece / 8);
+            const uint8_t* src = reinterpret_cast<const uint8_t*>(it.src);
+            const uint32_t n = it.bytes, lines = (n + 7) / 8;
+            if (it.seq == 0 && threadIdx.x == 0) st_ll(slot, it.pad, ~it.pad, flag);
+            for (uint32_t k = threadIdx.x; k < lines; k += blockDim.x) {
+                const uint32_t off = 8 * k, m = n - off < 8 ? n - off : 8;
+                const uint64_t v = load_upto8(src + off, m);
+                st_ll(lines0 + k, static_cast<uint32_t>(v), static_cast<uint32_t>(v >> 32), flag);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Every CTA, all threads, after its forwarding work: poll my LL slots and
+// decode them into the receive buffer.  A line is valid once both of its
+// 8-byte halves carry this epoch's flag.
+__device__ void ll_recv_all(const LaunchArgs& a) {
+    const CommDevice* c = a.comm;
+    const int me = c->rank, R = c->nranks;
+    const uint32_t flag = static_cast<uint32_t>(a.epoch);
+    const uint64_t limit = static_cast<uint64_t>(c->timeout_ms) * 1000000ull;
+    volatile uint32_t* status = c->status;
+    for (uint32_t j = blockIdx.x; j < a.n_ll_recv; j += gridDim.x) {
+        const Item it = a.ll_items[a.n_ll_send + j];
+        const int s = it.peer;
+        const uint4* slot =
+            reinterpret_cast<const uint4*>(c->ctrl[me] + FlagLayout::ll_off(R, static_cast<int>(a.epoch & 1), s));
+        const uint4* lines0 = slot + 1 + it.seq * (kLLPiece / 8);
+        uint8_t* dst = reinterpret_cast<uint8_t*>(it.dst);
+        const uint32_t n = it.bytes, lines = (n + 7) / 8;
+        // thread slot k = lines is piece 0's header check (line 0)
+        const uint32_t last = it.seq == 0 ? lines : lines - 1;
+        for (uint32_t k = threadIdx.x; k <= last; k += blockDim.x) {
+            const uint4* line = k == lines ? slot : lines0 + k;
+            uint4 v = ld_ll(line);
+            if (v.y != flag || v.w != flag) {
+                const uint64_t t0 = global_ns();
+                for (uint32_t spin = 0;; ++spin) {
+                    v = ld_ll(line);
+                    if (v.y == flag && v.w == flag) break;
+                    if ((spin & 255) == 255) {
+                        if (*status != 0) break;
+                        if (global_ns() - t0 > limit) {
+                            atomicCAS(c->status, 0u, static_cast<uint32_t>(kErrLLTimeout));
+                            break;
+                        }
+                    }
+                }
+                if (v.y != flag || v.w != flag) break;  // error latched
+            }
+            if (k == lines) {
+                if (v.x != it.pad || v.z != ~it.pad) atomicCAS(c->status, 0u, static_cast<uint32_t>(kErrSizeMismatch));
+            } else {
+                const uint32_t off = 8 * k, m = n - off < 8 ? n - off : 8;
+                store_upto8(dst + off, static_cast<uint64_t>(v.x) | static_cast<uint64_t>(v.z) << 32, m);
+            }
+        }
+    }
+}
+
 __device__ void produce(SharedState& sh, uint8_t* stages, const LaunchArgs& a) {
     uint32_t* scratch = a.comm->scratch;
     uint32_t cnt = 0, nsig = 0;
@@ -653,6 +768,7 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
     }
     __syncthreads();
     if (tid == 0 && blockIdx.x == 0) trace_max(a, kTracePrologueDone);
+    if (a.n_ll_send) ll_send_all(a);
 
     const int warp = tid / 32;
     if (warp == 0) {
@@ -663,6 +779,7 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
         consume(sh, stages, a);
     }
     __syncthreads();
+    if (a.n_ll_recv) ll_recv_all(a);
 
     // Epilogue.  done[me] / pulled[me] at every peer are per-pair counters that
     // gain exactly 2^32 per launch, so "epoch e complete" is counter >= e << 32:
@@ -702,6 +819,10 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
                 CtrlHeader* ph = reinterpret_cast<CtrlHeader*>(c->ctrl[lane]);
                 red_add_sys(&ph->done[me], ((a.write_targets >> lane) & 1) ? full - gridDim.x : full);
                 red_add_sys(&ph->pulled[me], ((a.pull_req >> lane) & 1) ? full - gridDim.x : full);
+                // this launch's LL slots are drained: acknowledged to every peer,
+                // LL sender now or not, so a sender's wait for epoch - 2 never
+                // depends on which pairs were small back then
+                st_relaxed(&ph->ll_ack[me], a.epoch);
             }
             __syncwarp();
             if (lane == 0) trace_max(a, kTraceSignalled);

@@ -48,8 +48,19 @@ constexpr double kHop2 = 1e-9;  // forward of chunk k sorts right after its stag
 
 }  // namespace
 
+bool ll_pair(const PlanResult& plan, int s, int d, uint64_t bytes, uint64_t ll_max) {
+    if (s == d || bytes == 0 || bytes > ll_max || bytes > kLLMaxData) return false;
+    for (const PairRoutes& pr : plan.pairs)
+        if (pr.src == s && pr.dst == d) {
+            for (const Flow& f : pr.flows)
+                if (pr.cands[static_cast<size_t>(f.cand)].route != Route::Direct) return false;
+            return true;
+        }
+    return true;  // not in the plan: a direct pair
+}
+
 Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t pipe_chunk, uint32_t slots,
-                        uint64_t direct_chunk, uint64_t push_chunk) {
+                        uint64_t direct_chunk, uint64_t push_chunk, uint64_t ll_max) {
     const int R = rb.R, me = rb.me;
     if (R > kMaxRanks) throw Error(nimbleInvalidArgument, "schedule: too many ranks");
     if (pipe_chunk == 0 || pipe_chunk > 0xffffffffull) throw Error(nimbleInvalidArgument, "schedule: bad pipe_chunk");
@@ -72,8 +83,35 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
         sc.moved_bytes += rb.send_bytes[me];
     }
 
+    std::vector<Item> ll_recv;
     for (const PairRoutes& pr : plan.pairs) {
         const int s = pr.src, d = pr.dst;
+        if ((s == me || d == me) && ll_pair(plan, s, d, pr.demand, ll_max)) {
+            if (s == me && pr.demand != rb.send_bytes[d])
+                throw Error(nimbleInvalidArgument, "schedule: plan demand differs from the send count");
+            if (d == me && pr.demand != rb.recv_bytes[s])
+                throw Error(nimbleInvalidArgument, "alltoallv: receive count differs from the planned demand");
+            for (uint64_t off = 0; off < pr.demand; off += kLLPiece) {  // pieces: several CTAs per pair
+                Item it{};
+                it.bytes = static_cast<uint32_t>(std::min<uint64_t>(kLLPiece, pr.demand - off));
+                it.seq = static_cast<uint32_t>(off / kLLPiece);
+                it.pad = static_cast<uint32_t>(pr.demand);
+                if (s == me) {
+                    it.kind = kLLSend;
+                    it.peer = static_cast<uint8_t>(d);
+                    it.src = rb.send_ptr[d] + off;
+                    sc.ll_items.push_back(it);
+                } else {
+                    it.kind = kLLRecv;
+                    it.peer = static_cast<uint8_t>(s);
+                    it.dst = rb.recv_ptr[s] + off;
+                    ll_recv.push_back(it);
+                }
+            }
+            if (s == me) sc.moved_bytes += pr.demand;
+            else sc.ll_senders |= 1ull << s;
+            continue;
+        }
         if (s != me && d != me) {
             // only relay duty can involve me
             bool relays_me = false;
@@ -161,6 +199,9 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
         }
     }
     sc.items = ordered(keyed);
+    sc.n_ll_send = static_cast<uint32_t>(sc.ll_items.size());
+    sc.n_ll_recv = static_cast<uint32_t>(ll_recv.size());
+    sc.ll_items.insert(sc.ll_items.end(), ll_recv.begin(), ll_recv.end());
     return sc;
 }
 

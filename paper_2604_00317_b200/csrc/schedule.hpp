@@ -33,6 +33,9 @@ struct RankBuffers {
 
 struct Schedule {
     std::vector<Item> items;
+    std::vector<Item> ll_items;  // LL sends, then LL receives (engine: LaunchArgs::ll_items)
+    uint32_t n_ll_send = 0, n_ll_recv = 0;
+    uint64_t ll_senders = 0;
     std::vector<Post> posts;
     std::vector<uint64_t> final_waits;  // (ctrl byte offset, chunk index) pairs
     std::vector<Post> send_posts;
@@ -49,7 +52,12 @@ struct Schedule {
 // and of local copies -- small enough that the last wave of items ends within
 // a few microseconds across CTAs.
 Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t pipe_chunk, uint32_t slots,
-                        uint64_t direct_chunk, uint64_t push_chunk = 0);
+                        uint64_t direct_chunk, uint64_t push_chunk = 0, uint64_t ll_max = 0);
+
+// Does pair (s, d) of `bytes` ride the LL protocol?  Both endpoints decide
+// alike from what they both know: the pair size and the replicated plan
+// (0 < bytes <= ll_max, no relay route).
+bool ll_pair(const PlanResult& plan, int s, int d, uint64_t bytes, uint64_t ll_max);
 
 // 1-GPU emulated exchange: every pair's segment as local copies (packed layout).
 std::vector<Item> build_local_items(int R, const uint64_t* matrix, const uint64_t* send_base,

@@ -329,6 +329,85 @@ def w_overtake(comm, rank, R, big):
     return int(bad.item())
 
 
+def w_ll(comm, rank, R):
+    """Low-latency protocol for pairs <= ll_max (64 KiB, cut into 8 KiB pieces):
+    odd sizes around the piece and pair thresholds next to normal pairs, unaligned packed offsets, six back-to-back
+    launches without a host sync (slot parity + acknowledgements), a CUDA graph
+    replaying an all-LL exchange, and the same traffic with LL disabled."""
+    from paper_2604_00317_b200 import comm as C
+    sizes = [1, 7, 8, 9, 8191, 8192, 8193, 40961, 65535, 65536, 65537, 1 << 20, 3]
+
+    def mat(shift):
+        return [0 if s == d else sizes[(3 * s + 5 * d + shift) % len(sizes)] for s in range(R) for d in range(R)]
+
+    out = []
+    for ll_max in (64 << 10, 0):
+        comm.set_config(ll_max=ll_max)
+        runs = []
+        for i in range(6):
+            m = mat(i % 2)
+            sc, sd, rc, rd = C.packed_displs(m, R, rank)
+            send = torch.empty(max(sum(sc), 16), dtype=torch.uint8, device="cuda")
+            recv = torch.full((max(sum(rc), 16),), 0xEE, dtype=torch.uint8, device="cuda")
+            for d in range(R):
+                C.fill_payload(send[sd[d]:], 0, sc[d], 60 + i, rank, d)
+            runs.append((sc, sd, rc, rd, send, recv))
+        torch.cuda.synchronize()
+        for sc, sd, rc, rd, send, recv in runs:  # no host sync in between
+            comm.alltoallv(send, sc, sd, recv, rc, rd)
+        torch.cuda.synchronize()
+        comm.check_async()
+        bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+        for i, (sc, sd, rc, rd, send, recv) in enumerate(runs):
+            for src in range(R):
+                C.check_payload(recv[rd[src]:], 0, rc[src], 60 + i, src, rank, bad)
+            if recv.numel() > sum(rc):
+                bad += int((recv[sum(rc):] != 0xEE).sum())
+        torch.cuda.synchronize()
+        out.append(int(bad.item()))
+    comm.set_config(ll_max=64 << 10)
+    # an all-LL exchange captured in a CUDA graph
+    m = [0 if s == d else 1000 + 13 * s + d for s in range(R) for d in range(R)]
+    sc, sd, rc, rd = C.packed_displs(m, R, rank)
+    send = torch.empty(sum(sc), dtype=torch.uint8, device="cuda")
+    recv = torch.zeros(sum(rc), dtype=torch.uint8, device="cuda")
+    comm.alltoallv(send, sc, sd, recv, rc, rd)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        comm.alltoallv(send, sc, sd, recv, rc, rd)
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for i in range(4):
+        for d in range(R):
+            C.fill_payload(send[sd[d]:], 0, sc[d], 90 + i, rank, d)
+        recv.zero_()
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        for src in range(R):
+            C.check_payload(recv[rd[src]:], 0, rc[src], 90 + i, src, rank, bad)
+    torch.cuda.synchronize()
+    comm.check_async()
+    out.append(int(bad.item()))
+    return out
+
+
+def w_ll_mismatch(comm, rank, R):
+    """LL-sized pair whose receiver expects one byte less: the header's byte
+    count turns it into an async error, not silent truncation."""
+    n = 4096
+    x = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    y = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    sc = [n if d != rank else 0 for d in range(R)]
+    rc = [n - (1 if rank == 1 and s == 0 else 0) if s != rank else 0 for s in range(R)]
+    try:
+        comm.alltoallv(x, sc, [0] * R, y, rc, [0] * R)
+        torch.cuda.synchronize()
+    except Exception as e:  # host-side detection is acceptable too
+        return "raised: " + str(e)[:60]
+    return comm.async_error()
+
+
 def w_bench(comm, rank, R):
     return comm.bench_skewed(32 * MiB, 0.7, 0, warmup=1, iters=3)
 
@@ -467,3 +546,16 @@ def test_comm_init_all_single_process_grouped():
 def test_receiver_two_launches_ahead_of_sender():
     out = _spawn("w_overtake", 2, 4 << 30)
     assert all(v == 0 for v in out.values()), out
+
+
+@need2
+def test_low_latency_protocol_small_pairs():
+    R = min(_ngpus(), 4)
+    out = _spawn("w_ll", R)
+    assert all(v == [0, 0, 0] for v in out.values()), out
+
+
+@need2
+def test_low_latency_size_mismatch_is_an_error():
+    out = _spawn("w_ll_mismatch", 2)
+    assert out[1] != 0, out  # the receiver that expected fewer bytes reports it

@@ -27,8 +27,10 @@ def main():
         comm.set_config(fabric="alltoall", gpus_per_node=R)
     for pull in [int(v) for v in os.environ.get("TRACE_PULL", "1,2").split(",")]:
         comm.set_config(pull=pull)
-        for mib in ((64, 1024) if case == "relay" else (1, 256)):
-            m = P.gen_p2p(R, 0, 1, mib * MiB) if case == "relay" else P.gen_skewed_a2av(R, mib * MiB, 0.7, 0)
+        sizes = [int(v) for v in os.environ.get("TRACE_KIB", "65536,1048576" if case == "relay" else "1024,262144").split(",")]
+        for kib in sizes:
+            mib = kib / 1024
+            m = P.gen_p2p(R, 0, 1, kib * 1024) if case == "relay" else P.gen_skewed_a2av(R, kib * 1024, 0.7, 0)
             sc, sd, rc, rd = C.packed_displs(m, R, rank)
             send = torch.empty(max(sum(sc), 16), dtype=torch.uint8, device="cuda")
             recv = torch.empty(max(sum(rc), 16), dtype=torch.uint8, device="cuda")
@@ -39,10 +41,9 @@ def main():
             allt = [None] * world
             dist.all_gather_object(allt, tr)
             if rank == 0:
-                t0 = min(t[0] for t in allt)
-                print(f"pull={pull} {mib}MiB (us from earliest kernel start; globaltimers assumed aligned)")
+                print(f"pull={pull} {kib} KiB/rank (us from each rank's own kernel start; globaltimers differ across GPUs)")
                 for r, t in enumerate(allt):
-                    print(f"  rank {r}: " + " ".join(f"{n}={(v - t0) / 1e3:8.1f}" for n, v in zip(NAMES, t[:8])),
+                    print(f"  rank {r}: " + " ".join(f"{n}={(v - t[0]) / 1e3:6.1f}" for n, v in zip(NAMES, t[:8])),
                           flush=True)
             comm.deregister(hs)
             comm.deregister(hr)
