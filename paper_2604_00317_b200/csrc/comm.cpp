@@ -635,6 +635,10 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     a.n_ll_recv = cs.sc.n_ll_recv;
     a.ll_items = cs.ll_items.p;
     a.ll_senders = cs.sc.ll_senders;
+    // Pulls keep at most 3 stages (96 KB) in flight per CTA: plenty for the
+    // link, and a shorter drain (c3 at 4 GPUs, r = 0.5: 0.726 -> 0.773 of the
+    // bound; other ratios within +-0.005; profiles/r01_pull_depth_n4.jsonl).
+    a.pull_depth = 3;
     a.local_only = 0;
     if (c->d_trace) {
         static const uint64_t init[kTraceSlots] = {~0ull, 0, ~0ull, 0, 0, 0, 0, ~0ull};

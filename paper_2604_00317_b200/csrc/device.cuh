@@ -166,6 +166,7 @@ struct LaunchArgs {
     const Item* ll_items;             // pieces of <= kLLPiece: kLLSend src / kLLRecv dst absolute, peer = the
                                       // other end, seq = piece index, pad = the pair's byte count
     uint64_t ll_senders;              // senders whose LL slot I drain this launch
+    uint32_t pull_depth;              // max stages in flight per CTA for a pull (kStages: no cap)
     uint32_t local_only;              // 1: flagless single-GPU exchange (no ctrl)
     uint64_t* trace;                  // optional globaltimer stamps (NIMBLE_TRACE=1), see kTrace*
 };

@@ -598,6 +598,14 @@ __device__ void produce(SharedState& sh, uint8_t* stages, const LaunchArgs& a) {
         for (uint64_t k = 0; k < nstages; ++k) {
             uint32_t slot;
             next_slot(slot);
+            // Remote (NVLink) sources need far less in flight than HBM copies
+            // (~16 KB per CTA covers the link's latency-bandwidth product): cap
+            // a pull at pull_depth outstanding stages so the drain at the end
+            // of the exchange stays short.
+            if (it.kind == kPull && a.pull_depth < kStages && cnt >= a.pull_depth) {
+                const uint32_t j = cnt - a.pull_depth;
+                mbar_wait(&sh.empty[j % kStages], (j / kStages) & 1);
+            }
             StageDesc& ds = sh.desc[slot];
             const uint64_t v0 = k * kStageVecs;
             const uint32_t nvec = static_cast<uint32_t>(n16 > v0 ? (n16 - v0 < kStageVecs ? n16 - v0 : kStageVecs) : 0);
@@ -720,20 +728,16 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
     SharedState& sh = *reinterpret_cast<SharedState*>(smem_raw);
     // The launch's epoch comes from device memory, not the host: a launch
     // captured in a CUDA graph and replayed gets a fresh epoch every time.
+    // Launched with programmatic stream serialization: this grid may start
+    // while the previous exchange on the stream is still finishing.  Everything
+    // up to griddepcontrol.wait touches only this CTA's shared memory.
     __shared__ LaunchArgs a;
-    if (threadIdx.x == 0) {
-        a = args;
-        a.epoch = args.local_only ? 0 : *reinterpret_cast<volatile uint64_t*>(args.comm->epoch) + 1;
-    }
-    __syncthreads();
+    if (threadIdx.x == 0) a = args;
     uint8_t* stages = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw + sizeof(SharedState)) + 127) & ~static_cast<uintptr_t>(127));
-    const CommDevice* c = a.comm;
+    const CommDevice* c = args.comm;  // the parameter, not the shared copy (not yet synced)
     const int tid = threadIdx.x;
-    uint32_t* scratch = c->scratch;
-    const int me = c->rank, R = c->nranks;
 
-    if (tid == 0) trace_min(a, kTraceKernelStart);
     for (int i = tid; i < kMaxRanks * kMaxRanks; i += kThreads) sh.seg_mode[i] = 0;
     for (int i = tid; i < kMaxRanks; i += kThreads) sh.send_mode[i] = 0;
     if (tid == 0) sh.remote_writes = 0;
@@ -748,6 +752,14 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // prior grids complete, their writes visible
+    if (tid == 0) {
+        a.epoch = a.local_only ? 0 : *reinterpret_cast<volatile uint64_t*>(c->epoch) + 1;
+        trace_min(a, kTraceKernelStart);
+    }
+    __syncthreads();
+    uint32_t* scratch = c->scratch;
+    const int me = c->rank, R = c->nranks;
     // Prologue: publish where each sender's segment lands in my buffer.
     if (!a.local_only && blockIdx.x == 0 && tid < 2 * R) {
         const bool send_side = tid >= R;
@@ -780,6 +792,7 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
     }
     __syncthreads();
     if (a.n_ll_recv) ll_recv_all(a);
+    if (tid == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // next exchange may start launching
 
     // Epilogue.  done[me] / pulled[me] at every peer are per-pair counters that
     // gain exactly 2^32 per launch, so "epoch e complete" is counter >= e << 32:
@@ -914,8 +927,17 @@ cudaError_t launch_exchange(const LaunchArgs& args, int ctas, cudaStream_t strea
         if (e != cudaSuccess) return e;
         configured_device = dev;
     }
-    exchange_kernel<<<ctas, kThreads, kEngineSmem, stream>>>(args);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(ctas));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kEngineSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap with the previous exchange's tail
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, exchange_kernel, args);
 }
 
 static int grid_for(uint64_t words) {

@@ -30,7 +30,12 @@ def main():
         sizes = [int(v) for v in os.environ.get("TRACE_KIB", "65536,1048576" if case == "relay" else "1024,262144").split(",")]
         for kib in sizes:
             mib = kib / 1024
-            m = P.gen_p2p(R, 0, 1, kib * 1024) if case == "relay" else P.gen_skewed_a2av(R, kib * 1024, 0.7, 0)
+            if case == "relay":
+                m = P.gen_p2p(R, 0, 1, kib * 1024)
+            elif case == "irregular":  # c4: total bytes over the whole matrix
+                m = P.gen_irregular(R, kib * 1024, 0.5, 1)
+            else:
+                m = P.gen_skewed_a2av(R, kib * 1024, 0.7, 0)
             sc, sd, rc, rd = C.packed_displs(m, R, rank)
             send = torch.empty(max(sum(sc), 16), dtype=torch.uint8, device="cuda")
             recv = torch.empty(max(sum(rc), 16), dtype=torch.uint8, device="cuda")
