@@ -315,7 +315,9 @@ nimbleResult_t nimbleDebugSchedule(nimblePlan_t plan, int rank, int ranks, uint6
 
 /* Device timeline of the comm's last launch (%globaltimer ns): kernel start,
  * prologue done, first item, last item, CTAs done, completions signalled,
- * completions observed.  Needs NIMBLE_TRACE=1 at comm creation; n >= 8. */
+ * completions observed, first CTA done, latest work loops done, latest
+ * completion fence, earliest work loops done (16 slots).  Needs NIMBLE_TRACE=1
+ * at comm creation; n >= 16. */
 nimbleResult_t nimbleCommDebugTrace(nimbleComm_t comm, uint64_t* out, int n);
 
 #ifdef __cplusplus

@@ -118,8 +118,8 @@ class Comm:
 
     def debug_trace(self):
         """Device timeline (ns) of the last launch; needs NIMBLE_TRACE=1."""
-        out = (c_u64 * 8)()
-        _lib.call("nimbleCommDebugTrace", self._h, out, 8)
+        out = (c_u64 * 16)()
+        _lib.call("nimbleCommDebugTrace", self._h, out, 16)
         return list(out)
 
     # -- registration

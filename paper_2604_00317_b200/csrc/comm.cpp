@@ -641,7 +641,7 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     a.pull_depth = 3;
     a.local_only = 0;
     if (c->d_trace) {
-        static const uint64_t init[kTraceSlots] = {~0ull, 0, ~0ull, 0, 0, 0, 0, ~0ull};
+        static const uint64_t init[kTraceSlots] = {~0ull, 0, ~0ull, 0, 0, 0, 0, ~0ull, 0, 0, ~0ull, 0, 0, 0, 0, 0};
         CUDA_TRY(cudaMemcpyAsync(c->d_trace, init, sizeof init, cudaMemcpyHostToDevice, st));
         a.trace = c->d_trace;
     }

@@ -181,7 +181,10 @@ enum TraceSlot : int {
     kTraceSignalled = 5,     // done / pulled published
     kTraceWaited = 6,        // all incoming completions observed
     kTraceFirstCtaDone = 7,  // min over CTAs: first CTA out of work
-    kTraceSlots = 8,
+    kTraceLoopsDoneMax = 8,  // max over CTAs: producer / consumers / signal warp finished
+    kTraceFenceDoneMax = 9,  // max over CTAs: completion fence done
+    kTraceLoopsDoneMin = 10, // min over CTAs: loops finished
+    kTraceSlots = 16,
 };
 
 }  // namespace nb

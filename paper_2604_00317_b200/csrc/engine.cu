@@ -791,6 +791,10 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
         consume(sh, stages, a);
     }
     __syncthreads();
+    if (tid == 0) {
+        trace_max(a, kTraceLoopsDoneMax);
+        trace_min(a, kTraceLoopsDoneMin);
+    }
     if (a.n_ll_recv) ll_recv_all(a);
     if (tid == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // next exchange may start launching
 
@@ -809,9 +813,11 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
         if (tid == 0) {
             // this CTA's peer writes before its completion adds (pulls and local
             // copies only read remote memory: a GPU-scope fence will do)
-            if (sh.remote_writes) __threadfence_system();
-            else __threadfence();
+            // release (not sequentially consistent) fences: all the adds below need
+            if (sh.remote_writes) asm volatile("fence.acq_rel.sys;" ::: "memory");
+            else asm volatile("fence.acq_rel.gpu;" ::: "memory");
             trace_min(a, kTraceFirstCtaDone);
+            trace_max(a, kTraceFenceDoneMax);
         }
         __syncwarp();
         if (!a.local_only && tid < R) {
