@@ -585,10 +585,7 @@ CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& 
     c->fast.cs = nullptr;  // entries may be recycled below
     CachedSchedule cs;
     cs.key = key;
-    const char* env = std::getenv("NIMBLE_DIRECT_CHUNK");
-    const uint64_t dchunk = c->cfg.direct_chunk ? c->cfg.direct_chunk
-                            : env && *env          ? std::strtoull(env, nullptr, 0)
-                                                   : kDefaultDirectChunk;
+    const uint64_t dchunk = c->cfg.direct_chunk ? c->cfg.direct_chunk : kDefaultDirectChunk;
     cs.sc = build_schedule(plan, rb, c->cfg.pipe_chunk, slot_count(c->cfg), dchunk,
                            c->cfg.push_chunk ? c->cfg.push_chunk : kDefaultPushChunk, c->cfg.ll_max);
     if (c->schedules.size() >= 4) {  // recycle the oldest entry's device buffers

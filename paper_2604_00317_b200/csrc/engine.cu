@@ -1,22 +1,21 @@
 // The forwarding engine: one persistent sm_100a kernel per rank per exchange.
 //
-// Each CTA is warp-specialized:
-//   warp 0, lane 0  -- producer: pulls 32-byte work items from the rank's chunk
-//                      schedule in order (one atomicAdd per item), resolves
-//                      where the bytes go (receiver posts, staging slots),
-//                      performs the item's flag waits, and streams the source
-//                      bytes into a ring of shared-memory stages with TMA bulk
-//                      copies (cp.async.bulk global->shared, mbarrier
-//                      complete_tx) -- loads run NS stages ahead with no
-//                      register cost;
-//   warps 1..15     -- consumers: per stage, realign the bytes (source and
+// Each CTA (512 threads) is warp-specialized:
+//   warp 0, lane 0  -- producer: takes 32-byte work items from the rank's chunk
+//                      schedule in key order (one atomicAdd per item), resolves
+//                      where the bytes go (posts, staging slots), performs the
+//                      item's flag waits, and streams the source into a ring of
+//                      6 x 32 KB shared-memory stages with TMA bulk copies
+//                      (cp.async.bulk global->shared, mbarrier complete_tx);
+//                      pulls keep at most 3 stages in flight;
+//   warps 1..14     -- consumers: per stage, realign the bytes (source and
 //                      destination may be misaligned relative to each other:
 //                      two 16-byte shared loads + funnel shifts) and store them
-//                      with 16-byte coalesced st.global to the destination --
-//                      local HBM, a peer's registered buffer or a peer's
-//                      staging slot over NVLink; on an item's last stage one
-//                      consumer raises the item's flag (ready / consumed /
-//                      done) after a system-scope fence.
+//                      with 16-byte coalesced st.global -- to local HBM, a
+//                      peer's registered buffer or a peer's staging slot;
+//   warp 15         -- signal warp: raises item-end ready / consumed flags in
+//                      item order (system fence + relaxed stores), off the data
+//                      path.
 // Items are:
 //   kLocal   - local copy (self segment, and the 1-GPU emulated exchange);
 //   kPush    - direct push into the receiver's registered buffer over NVLink,
@@ -25,17 +24,27 @@
 //   kForward - relay hop 2 (or the receiver's drain of its self ring):
 //              staging slot -> final buffer;
 //   kPull    - receiver-driven direct flow: TMA bulk loads straight out of the
-//              sender's registered send buffer over NVLink (an ingress-heavy
-//              receiver asks, a registered sender grants and skips its pushes).
-// Flags follow the reference's bounded-buffer recurrence
-// (proj/src/pipeline.cpp:97-106; device.cuh).  Waits are polled by the
-// producer thread with acquire loads and a global-timer timeout that raises an
-// async error instead of hanging the GPU.
+//              sender's registered send buffer over NVLink (a receiver asks, a
+//              registered sender grants unless its own port is ingress-bound);
+//   LL       - small direct pairs (<= ll_max) bypass all of the above: the
+//              sender stores data + epoch flags into the receiver's LL slot at
+//              kernel start, the receiver polls and decodes at the end.
+// Posts (where a segment lands / lives) are pushed by their writer into the
+// reader's ctrl region at kernel start; completions are per-pair counters
+// (done / pulled) that gain exactly 2^32 per launch: each CTA adds 1 after
+// fencing its own writes, the last CTA adds the rest and waits for its peers.
+// Ring flags follow the reference's bounded-buffer recurrence
+// (proj/src/pipeline.cpp:97-106; device.cuh).  Every wait polls with acquire
+// loads and a global-timer timeout that latches an async error instead of
+// hanging the GPU.  Kernels are launched with programmatic stream
+// serialization: the next exchange's setup overlaps this one's tail and waits
+// (griddepcontrol.wait) before reading the launch epoch.
 //
 // Deadlock freedom: the scheduler sorts every rank's items by a global key
 // (chunk progress fraction), every wait targets an item with a strictly
 // smaller key, and items are taken in key order -- so the globally smallest
-// unfinished item always has its dependencies met.
+// unfinished item always has its dependencies met.  LL sends wait only for
+// the receiver's previous-but-one launch; LL receives only for LL sends.
 #include <cuda_runtime.h>
 
 #include <cstdint>
