@@ -16,6 +16,10 @@
 //   transfer  -> simulate_transfer (+ trace)     (proj/src/pipeline.cpp:66-116)
 //   topology  -> build_canonical link inventory  (proj/src/topology.cpp:119-179)
 //   exact     -> solve_exact                     (proj/src/oracle.cpp:67-91)
+//   calibrate -> calibrate with given targets    (proj/src/calibration.cpp:54-100)
+//   multipath -> intra_multipath_speedup         (proj/src/calibration.cpp:11-23)
+#include "nimble/calibration.hpp"
+
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -131,6 +135,30 @@ json plan_doc(const Topology& topo, const Plan& p) {
 json run(const json& req) {
     std::string op = req.at("op").get<std::string>();
     json out;
+    if (op == "calibrate") {  // calibrate() with caller-supplied targets (proj/src/calibration.cpp:54-100)
+        CalibrationTargets t;
+        const json& q = req.at("targets");
+        t.one_intermediate = q.value("one_intermediate", t.one_intermediate);
+        t.two_intermediate = q.value("two_intermediate", t.two_intermediate);
+        t.four_rail = q.value("four_rail", t.four_rail);
+        t.message = q.value("message", t.message);
+        t.nvlink_gbps = q.value("nvlink_gbps", t.nvlink_gbps);
+        t.rail_gbps = q.value("rail_gbps", t.rail_gbps);
+        CalibrationResult r = calibrate(t);
+        out["hop_latency"] = r.config.hop_latency;
+        out["pi"] = r.pi;
+        out["one_intermediate"] = r.one_intermediate;
+        out["two_intermediate"] = r.two_intermediate;
+        out["four_rail"] = r.four_rail;
+        return out;
+    }
+    if (op == "multipath") {  // intra_multipath_speedup (proj/src/calibration.cpp:11-23)
+        PipelineConfig cfg;
+        cfg.hop_latency = req.value("hop_latency", cfg.hop_latency);
+        out["speedup"] = intra_multipath_speedup(req.at("intermediates").get<int>(), req.at("message").get<std::uint64_t>(),
+                                                 req.at("nvlink_gbps").get<double>(), cfg);
+        return out;
+    }
     if (op == "topology") {
         Topology t = topo_from(req.at("topology"));
         json links = json::array();

@@ -8,6 +8,7 @@ the same buffers, relay flows, delivery mismatches.
   c4  irregular seeded matrix (seed 1, sparsity 0.5), total 1 KiB .. 1 GiB
   c1  p2p 64 MiB 0 -> 1 (W = 3: one relay GPU under the mesh model)
   c2  p2p 1 GiB 0 -> 1 (W = 4: two relay GPUs under the mesh model)
+  cal p2p 256 MiB 0 -> 1, direct and through W - 2 relays (calibration targets)
 SWEEP_CASES selects (default all that fit W).
 """
 import json
@@ -138,6 +139,9 @@ def sweep(comm, pg, rank, world, chunk):
         while t <= 1 << 30:
             run_point(comm, pg, rank, R, P.gen_irregular(R, t, 0.5, 1), "c4", extra={"total": t})
             t *= 16
+    if "cal" in cases and R >= 3:  # calibration points: p2p 256 MiB direct vs R-2 relays (mesh plan)
+        for fab in ("nvswitch", "alltoall"):
+            run_point(comm, pg, rank, R, P.gen_p2p(R, 0, 1, 256 * MiB), "cal", fab, extra={"per_rank": 256 * MiB})
     if "c1" in cases and R == 3:
         for fab in ("nvswitch", "alltoall"):
             run_point(comm, pg, rank, R, P.gen_p2p(R, 0, 1, 64 * MiB), "c1", fab)
