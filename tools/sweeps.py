@@ -2,7 +2,9 @@
 
 For the world size it is launched with (W), rank 0 prints one JSON line per
 point: nimble GB/s, fraction of the MCF port bound, NCCL all_to_all_single on
-the same buffers, relay flows, delivery mismatches.
+the same buffers, relay flows, delivery mismatches.  Times: 5 warm-up + 100
+timed rounds (SWEEP_ITERS), per-round CUDA events, max over ranks per round;
+`us` is the median, `us_min` / `us_mean` beside it.
   c3  skewed all-to-allv, 256 MiB/rank, hotspot ratio 0.0 .. 0.9
   c5  uniform all-to-allv (ratio 1/(W-1)), 256 MiB/rank
   c4  irregular seeded matrix (seed 1, sparsity 0.5), total 1 KiB .. 1 GiB
@@ -36,7 +38,28 @@ def port_bound(m, R):
                for v in range(R)) / 900e9
 
 
-def _run_point(comm, pg, rank, R, m, name, fabric="nvswitch", iters=10, warmup=3, nccl=True, extra=None):
+def timed(fn, st, iters, warmup):
+    """Per-iteration device times (CUDA events on `st`), max over ranks per
+    iteration; returns (median, min, mean) seconds.  Protocol of the
+    reference's bench (5 warm-up + 100 timed rounds)."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(iters + 1)]
+    ev[0].record(st)
+    for i in range(iters):
+        fn()
+        ev[i + 1].record(st)
+    torch.cuda.synchronize()
+    per = torch.tensor([ev[i].elapsed_time(ev[i + 1]) * 1e-3 for i in range(iters)], dtype=torch.float64)
+    dist.all_reduce(per, op=dist.ReduceOp.MAX)
+    v = sorted(per.tolist())
+    return v[len(v) // 2], v[0], sum(v) / len(v)
+
+
+def _run_point(comm, pg, rank, R, m, name, fabric="nvswitch", iters=None, warmup=5, nccl=True, extra=None):
+    iters = iters or int(os.environ.get("SWEEP_ITERS", "100"))
     comm.set_config(fabric=fabric, gpus_per_node=R)
     sc, sd, rc, rd = C.packed_displs(m, R, rank)
     send = torch.empty(max(sum(sc), 16), dtype=torch.uint8, device="cuda")
@@ -45,17 +68,7 @@ def _run_point(comm, pg, rank, R, m, name, fabric="nvswitch", iters=10, warmup=3
         C.fill_payload(send[sd[d]:], 0, sc[d], 9, rank, d)
     hs, hr = comm.register(send), comm.register(recv)
     st = torch.cuda.current_stream()
-    for _ in range(warmup):
-        comm.alltoallv(send, sc, sd, recv, rc, rd, st)
-    torch.cuda.synchronize()
-    dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    for _ in range(iters):
-        comm.alltoallv(send, sc, sd, recv, rc, rd, st)
-    e1.record(st)
-    torch.cuda.synchronize()
-    t = max_over(e0.elapsed_time(e1) * 1e-3 / iters)
+    t, t_min, t_mean = timed(lambda: comm.alltoallv(send, sc, sd, recv, rc, rd, st), st, iters, warmup)
     comm.check_async()
     bad = torch.zeros(1, dtype=torch.int64, device="cuda")
     for s in range(R):
@@ -66,17 +79,7 @@ def _run_point(comm, pg, rank, R, m, name, fabric="nvswitch", iters=10, warmup=3
     if nccl:
         out = torch.empty_like(recv)
         sv, rv = send[:sum(sc)], out[:sum(rc)]
-        for _ in range(warmup):
-            dist.all_to_all_single(rv, sv, list(rc), list(sc), group=pg)
-        torch.cuda.synchronize()
-        dist.barrier()
-        n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n0.record()
-        for _ in range(iters):
-            dist.all_to_all_single(rv, sv, list(rc), list(sc), group=pg)
-        n1.record()
-        torch.cuda.synchronize()
-        tn = max_over(n0.elapsed_time(n1) * 1e-3 / iters)
+        tn, _, _ = timed(lambda: dist.all_to_all_single(rv, sv, list(rc), list(sc), group=pg), st, iters, warmup)
     comm.deregister(hs)
     comm.deregister(hr)
     total = sum(m)
@@ -86,6 +89,7 @@ def _run_point(comm, pg, rank, R, m, name, fabric="nvswitch", iters=10, warmup=3
         t_ = P.build_canonical(1, R, 0, 900e9, 0, P.ALLTOALL)
         relays = sum(1 for pp in P.plan(t_, R, R, m).pairs for c, _ in pp.flows if c > 0)
     row = {"case": name, "ranks": R, "fabric_model": fabric, "total_bytes": total, "us": t * 1e6,
+           "us_min": t_min * 1e6, "us_mean": t_mean * 1e6, "iters": iters, "warmup": warmup,
            "gbps": total / t / 1e9, "bound_us": bound * 1e6, "frac_of_bound": bound / t if t else None,
            "nccl_us": tn * 1e6 if tn else None, "nccl_gbps": total / tn / 1e9 if tn else None,
            "vs_nccl": (tn / t) if tn else None, "relay_flows": relays, "mismatched_bytes": mism}
@@ -147,7 +151,7 @@ def sweep(comm, pg, rank, world, chunk):
             run_point(comm, pg, rank, R, P.gen_p2p(R, 0, 1, 64 * MiB), "c1", fab)
     if "c2" in cases and R == 4:
         for fab in ("nvswitch", "alltoall"):
-            run_point(comm, pg, rank, R, P.gen_p2p(R, 0, 1, 1 << 30), "c2", fab, iters=5)
+            run_point(comm, pg, rank, R, P.gen_p2p(R, 0, 1, 1 << 30), "c2", fab, iters=20)
 
 
 if __name__ == "__main__":
