@@ -330,18 +330,18 @@ def w_overtake(comm, rank, R, big):
 
 
 def w_ll(comm, rank, R):
-    """Low-latency protocol for pairs <= ll_max (64 KiB, cut into 8 KiB pieces):
+    """Low-latency protocol for pairs <= ll_max (256 KiB, cut into 8 KiB pieces):
     odd sizes around the piece and pair thresholds next to normal pairs, unaligned packed offsets, six back-to-back
     launches without a host sync (slot parity + acknowledgements), a CUDA graph
     replaying an all-LL exchange, and the same traffic with LL disabled."""
     from paper_2604_00317_b200 import comm as C
-    sizes = [1, 7, 8, 9, 8191, 8192, 8193, 40961, 65535, 65536, 65537, 1 << 20, 3]
+    sizes = [1, 7, 8, 9, 8191, 8192, 8193, 40961, 65535, 65536, 65537, 262144, 262145, 1 << 20, 3]
 
     def mat(shift):
         return [0 if s == d else sizes[(3 * s + 5 * d + shift) % len(sizes)] for s in range(R) for d in range(R)]
 
     out = []
-    for ll_max in (64 << 10, 0):
+    for ll_max in (256 << 10, 64 << 10, 0):
         comm.set_config(ll_max=ll_max)
         runs = []
         for i in range(6):
@@ -552,7 +552,7 @@ def test_receiver_two_launches_ahead_of_sender():
 def test_low_latency_protocol_small_pairs():
     R = min(_ngpus(), 4)
     out = _spawn("w_ll", R)
-    assert all(v == [0, 0, 0] for v in out.values()), out
+    assert all(v == [0, 0, 0, 0] for v in out.values()), out
 
 
 @need2

@@ -111,6 +111,8 @@ def main():
     comm = C.Comm.init_rank(world, uid[0], rank)
     if os.environ.get("SWEEP_PULL"):
         comm.set_config(pull=int(os.environ["SWEEP_PULL"]))
+    if os.environ.get("SWEEP_LL_MAX"):
+        comm.set_config(ll_max=int(os.environ["SWEEP_LL_MAX"]))
     for chunk in [int(v) for v in os.environ.get("SWEEP_CHUNKS", "0").split(",")]:
         comm.set_config(direct_chunk=chunk)
         sweep(comm, pg, rank, world, chunk)
@@ -138,6 +140,10 @@ def sweep(comm, pg, rank, world, chunk):
             run_point(comm, pg, rank, R, m, "c3a", extra={"ratio": i / 10, "per_rank": per_rank})
     if "c5" in cases:
         run_point(comm, pg, rank, R, P.gen_skewed_a2av(R, 256 * MiB, 1.0 / (R - 1), 0), "c5")
+    if "c3k" in cases:  # small skewed exchanges: 64 KiB .. 4 MiB per rank, r = 0.7
+        for kib in (64, 256, 1024, 4096):
+            run_point(comm, pg, rank, R, P.gen_skewed_a2av(R, kib << 10, 0.7, 0), "c3k",
+                      extra={"ratio": 0.7, "per_rank": kib << 10})
     if "c4" in cases:
         t = 1024
         while t <= 1 << 30:
