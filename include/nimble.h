@@ -234,6 +234,10 @@ nimbleResult_t nimbleCommDeregister(const nimbleComm_t comm, void* handle);
 nimbleResult_t nimbleMemAlloc(void** ptr, size_t size);
 nimbleResult_t nimbleMemFree(void* ptr);
 
+/* Group semantics follow NCCL (ops are enqueued, one exchange per comm is
+ * launched at GroupEnd), with one restriction: a group may hold at most one
+ * send to and one receive from each peer (each pair is one contiguous
+ * segment); a second one is an nimbleInvalidUsage error, not a queued op. */
 nimbleResult_t nimbleGroupStart(void);
 nimbleResult_t nimbleGroupEnd(void);
 nimbleResult_t nimbleSend(const void* sendbuff, size_t count, nimbleDataType_t datatype, int peer,

@@ -408,6 +408,51 @@ def w_ll_mismatch(comm, rank, R):
     return comm.async_error()
 
 
+def w_sendrecv_mixed(comm, rank, R):
+    """One group with sends to two different peers: an LL-sized message to the
+    right neighbour, a normal-path one to the left, and a zero-byte one;
+    several rounds back to back with different sizes."""
+    from paper_2604_00317_b200 import comm as C
+    right, left = (rank + 1) % R, (rank - 1) % R
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    if R == 2:  # one peer: an LL-sized message one way, a normal-path one back
+        for it, (small, big) in enumerate([(3, 300001), (262144, 262145)]):
+            n_out, n_in = (small, big) if rank == 0 else (big, small)
+            x = torch.empty(n_out, dtype=torch.uint8, device="cuda")
+            C.fill_payload(x, 0, n_out, 500 + it, rank, 1 - rank)
+            y = torch.zeros(n_in, dtype=torch.uint8, device="cuda")
+            with C.group():
+                comm.send(x, n_out, 1 - rank)
+                comm.recv(y, n_in, 1 - rank)
+            torch.cuda.synchronize()
+            comm.check_async()
+            C.check_payload(y, 0, n_in, 500 + it, 1 - rank, rank, bad)
+        torch.cuda.synchronize()
+        return int(bad.item())
+    for it, (small, big) in enumerate([(3, 300001), (8192 + 5, 2 * MiB + 1), (262144, 262145)]):
+        xs = torch.empty(small, dtype=torch.uint8, device="cuda")
+        xb = torch.empty(big, dtype=torch.uint8, device="cuda")
+        C.fill_payload(xs, 0, small, 300 + it, rank, right)
+        C.fill_payload(xb, 0, big, 400 + it, rank, left)
+        ys = torch.zeros(small, dtype=torch.uint8, device="cuda")
+        yb = torch.zeros(big, dtype=torch.uint8, device="cuda")
+        z = torch.zeros(16, dtype=torch.uint8, device="cuda")
+        with C.group():
+            comm.send(xs, small, right)
+            comm.send(xb, big, left)
+            comm.recv(ys, small, left)    # left neighbour's small message is for me
+            comm.recv(yb, big, right)     # right neighbour's big message is for me
+            if R > 3:
+                comm.send(z, 0, (rank + 2) % R)
+                comm.recv(z, 0, (rank - 2) % R)
+        torch.cuda.synchronize()
+        comm.check_async()
+        C.check_payload(ys, 0, small, 300 + it, left, rank, bad)
+        C.check_payload(yb, 0, big, 400 + it, right, rank, bad)
+    torch.cuda.synchronize()
+    return int(bad.item())
+
+
 def w_bench(comm, rank, R):
     return comm.bench_skewed(32 * MiB, 0.7, 0, warmup=1, iters=3)
 
@@ -559,3 +604,10 @@ def test_low_latency_protocol_small_pairs():
 def test_low_latency_size_mismatch_is_an_error():
     out = _spawn("w_ll_mismatch", 2)
     assert out[1] != 0, out  # the receiver that expected fewer bytes reports it
+
+
+@need2
+def test_sendrecv_group_mixed_sizes_and_peers():
+    R = min(_ngpus(), 4)
+    out = _spawn("w_sendrecv_mixed", R)
+    assert all(v == 0 for v in out.values()), out
