@@ -58,6 +58,27 @@ def timed(fn, st, iters, warmup):
     return v[len(v) // 2], v[0], sum(v) / len(v)
 
 
+def timed_graph(fn, st, iters, warmup):
+    """`iters` calls captured in one CUDA graph, replayed once: per-call device
+    time without host launch overhead (max over ranks).  Returns seconds."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        for _ in range(iters):
+            fn()
+    g.replay()  # warm replay
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    g.replay()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return max_over(e0.elapsed_time(e1) * 1e-3 / iters)
+
+
 def _run_point(comm, pg, rank, R, m, name, fabric="nvswitch", iters=None, warmup=5, nccl=True, extra=None):
     iters = iters or int(os.environ.get("SWEEP_ITERS", "100"))
     comm.set_config(fabric=fabric, gpus_per_node=R)
@@ -80,6 +101,15 @@ def _run_point(comm, pg, rank, R, m, name, fabric="nvswitch", iters=None, warmup
         out = torch.empty_like(recv)
         sv, rv = send[:sum(sc)], out[:sum(rc)]
         tn, _, _ = timed(lambda: dist.all_to_all_single(rv, sv, list(rc), list(sc), group=pg), st, iters, warmup)
+    graph = None
+    if os.environ.get("SWEEP_GRAPH") == "1":  # host overhead removed, both arms
+        st2 = torch.cuda.Stream()
+        with torch.cuda.stream(st2):
+            graph = {"nimble_us": timed_graph(lambda: comm.alltoallv(send, sc, sd, recv, rc, rd, st2), st2, iters,
+                                              warmup) * 1e6}
+            if nccl:
+                graph["nccl_us"] = timed_graph(lambda: dist.all_to_all_single(rv, sv, list(rc), list(sc), group=pg),
+                                               st2, iters, warmup) * 1e6
     comm.deregister(hs)
     comm.deregister(hr)
     total = sum(m)
@@ -93,6 +123,8 @@ def _run_point(comm, pg, rank, R, m, name, fabric="nvswitch", iters=None, warmup
            "gbps": total / t / 1e9, "bound_us": bound * 1e6, "frac_of_bound": bound / t if t else None,
            "nccl_us": tn * 1e6 if tn else None, "nccl_gbps": total / tn / 1e9 if tn else None,
            "vs_nccl": (tn / t) if tn else None, "relay_flows": relays, "mismatched_bytes": mism}
+    if graph:
+        row["graph"] = graph
     if extra:
         row.update(extra)
     if rank == 0:
