@@ -536,6 +536,7 @@ __device__ void ll_recv_all(const LaunchArgs& a) {
                             break;
                         }
                     }
+                    if (spin > 16) __nanosleep(64);  // thousands of pollers: keep L2 free for the incoming lines
                 }
                 if (v.y != flag || v.w != flag) break;  // error latched
             }
