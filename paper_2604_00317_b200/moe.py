@@ -5,7 +5,10 @@ experts that live on other ranks, and a skewed router turns the dispatch into
 exactly the skewed all-to-allv this library accelerates.  This module is the
 upstream caller: the byte movement is
 `Comm.alltoallv` (the sm_100a forwarding engine); PyTorch only does the index
-bookkeeping around it (argsort / gather / index_add).
+bookkeeping around it (argsort / gather / index_add).  Two faces:
+`MoEDispatcher` (registered staging buffers, zero copy, inference) and the
+`nimble_b200::alltoallv_rows` custom operator with autograd behind the
+differentiable `dispatch` / `combine` functions (training).
 
 Layout: experts are block-distributed, expert e lives on rank e // E_local.
 dispatch() sends every (token, k) assignment's hidden vector to its expert's
@@ -117,4 +120,87 @@ class MoEDispatcher:
         return out
 
 
-__all__ = ["MoEDispatcher", "DispatchHandle", "_lib"]
+# ---------------------------------------------------------------- custom op
+#
+# The same exchange as a PyTorch custom operator with autograd, so a training
+# step can differentiate through dispatch / combine: the backward of an
+# all-to-allv of rows is the all-to-allv of the row gradients the other way.
+
+_COMMS: dict = {}
+
+
+def comm_id(comm: Comm) -> int:
+    """Integer handle of `comm` for the custom op (custom ops take no Python objects)."""
+    _COMMS[id(comm)] = comm
+    return id(comm)
+
+
+def _prefix(counts):
+    out, acc = [], 0
+    for c in counts:
+        out.append(acc)
+        acc += c
+    return out
+
+
+@torch.library.custom_op("nimble_b200::alltoallv_rows", mutates_args=())
+def alltoallv_rows(x: torch.Tensor, send_counts: list[int], recv_counts: list[int], comm: int) -> torch.Tensor:
+    """x [sum(send_counts), ...] rows grouped by destination rank -> [sum(recv_counts), ...]
+    grouped by source rank, through the forwarding engine (nimbleAlltoAllv) on the
+    current stream."""
+    c = _COMMS[comm]
+    x = x.contiguous()
+    row = x[0].numel() * x.element_size() if x.shape[0] else int(torch.tensor(x.shape[1:]).prod()) * x.element_size()
+    out = x.new_empty((sum(recv_counts),) + tuple(x.shape[1:]))
+    sb = [n * row for n in send_counts]
+    rb = [n * row for n in recv_counts]
+    c.alltoallv(x, sb, _prefix(sb), out, rb, _prefix(rb))
+    return out
+
+
+@alltoallv_rows.register_fake
+def _alltoallv_rows_fake(x, send_counts, recv_counts, comm):
+    return x.new_empty((sum(recv_counts),) + tuple(x.shape[1:]))
+
+
+def _a2a_setup(ctx, inputs, output):
+    _, ctx.send_counts, ctx.recv_counts, ctx.comm = inputs
+
+
+def _a2a_backward(ctx, grad):
+    return alltoallv_rows(grad.contiguous(), ctx.recv_counts, ctx.send_counts, ctx.comm), None, None, None
+
+
+alltoallv_rows.register_autograd(_a2a_backward, setup_context=_a2a_setup)
+
+
+def dispatch(comm: Comm, x: torch.Tensor, topk_ids: torch.Tensor, num_experts: int):
+    """Differentiable dispatch: x [T, H], topk_ids [T, k] -> (recv_x [N, H], recv_expert [N] local
+    ids, handle).  Rows are grouped by destination rank, (token, k) order within."""
+    R = comm.nranks
+    epr = num_experts // R
+    T, k = topk_ids.shape
+    flat = topk_ids.reshape(-1).to(torch.int64)
+    dest = flat // epr
+    order = torch.argsort(dest, stable=True)
+    count_out = torch.bincount(dest, minlength=R)
+    count_in = torch.empty_like(count_out)
+    comm.alltoall(count_out, count_in, 8)
+    sc, rc = count_out.tolist(), count_in.tolist()
+    cid = comm_id(comm)
+    recv_x = alltoallv_rows(x.index_select(0, order // k), sc, rc, cid)
+    recv_e = alltoallv_rows((flat[order] % epr).to(torch.int32).unsqueeze(1), sc, rc, cid).squeeze(1)
+    return recv_x, recv_e, DispatchHandle(order, sc, rc, T, k)
+
+
+def combine(comm: Comm, y: torch.Tensor, handle: DispatchHandle, weights: torch.Tensor | None = None):
+    """Differentiable combine: y [N, H] in dispatch-receive order -> out [T, H], the
+    router-weighted sum over each token's k assignments."""
+    back = alltoallv_rows(y, handle.recv_counts, handle.send_counts, comm_id(comm))
+    if weights is not None:
+        back = back * weights.reshape(-1)[handle.order].to(back.dtype).unsqueeze(1)
+    out = torch.zeros(handle.num_tokens, y.shape[1], dtype=y.dtype, device=y.device)
+    return out.index_add(0, handle.order // handle.topk, back)
+
+
+__all__ = ["MoEDispatcher", "DispatchHandle", "alltoallv_rows", "dispatch", "combine", "comm_id", "_lib"]

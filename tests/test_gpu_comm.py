@@ -453,6 +453,34 @@ def w_sendrecv_mixed(comm, rank, R):
     return int(bad.item())
 
 
+def w_moe_autograd(comm, rank, R):
+    """Differentiable dispatch / combine through the nimble_b200::alltoallv_rows
+    custom op: forward and the gradients of x and of the router weights match
+    the same computation done locally (fp32)."""
+    from paper_2604_00317_b200 import moe
+    g = torch.Generator(device="cuda").manual_seed(200 + rank)
+    T, H, k, E = 513, 64, 2, 4 * R
+    x = torch.randn(T, H, device="cuda", generator=g, requires_grad=True)
+    w = torch.rand(T, k, device="cuda", generator=g, requires_grad=True)
+    hot = torch.rand(T, k, device="cuda", generator=g) < 0.6
+    ids = torch.where(hot, torch.zeros_like(hot, dtype=torch.int64),
+                      torch.randint(0, E, (T, k), device="cuda", generator=g))
+    gout = torch.randn(T, H, device="cuda", generator=g)
+    epr = E // R
+    recv_x, recv_e, h = moe.dispatch(comm, x, ids, E)
+    y = recv_x * (recv_e.to(torch.float32) + rank * epr + 1).unsqueeze(1)
+    out = moe.combine(comm, y, h, w)
+    (out * gout).sum().backward()
+    torch.cuda.synchronize()
+    comm.check_async()
+    x2, w2 = x.detach().clone().requires_grad_(True), w.detach().clone().requires_grad_(True)
+    ref = (x2.unsqueeze(1) * (ids.to(torch.float32) + 1).unsqueeze(2) * w2.unsqueeze(2)).sum(1)
+    (ref * gout).sum().backward()
+    ok = (torch.allclose(out, ref, rtol=1e-5, atol=1e-5) and torch.allclose(x.grad, x2.grad, rtol=1e-5, atol=1e-5)
+          and torch.allclose(w.grad, w2.grad, rtol=1e-4, atol=1e-4))
+    return bool(ok), sum(h.recv_counts)
+
+
 def w_bench(comm, rank, R):
     return comm.bench_skewed(32 * MiB, 0.7, 0, warmup=1, iters=3)
 
@@ -611,3 +639,10 @@ def test_sendrecv_group_mixed_sizes_and_peers():
     R = min(_ngpus(), 4)
     out = _spawn("w_sendrecv_mixed", R)
     assert all(v == 0 for v in out.values()), out
+
+
+@need2
+def test_moe_custom_op_forward_and_gradients():
+    R = min(_ngpus(), 4)
+    res = _spawn("w_moe_autograd", R)
+    assert all(ok for ok, _ in res.values()), res
