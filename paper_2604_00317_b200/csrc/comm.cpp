@@ -252,6 +252,10 @@ struct nimbleComm {
     cudaEvent_t last_launch = nullptr;  // launches on one comm are serialized across streams
     cudaStream_t last_stream = nullptr;
     bool launched = false;
+    // Frees whatever device / host state exists, so a comm whose init failed
+    // half-way releases what it had allocated (nimbleCommDestroy first makes
+    // sure no peer still touches it).
+    ~nimbleComm();
 };
 
 namespace nb {
@@ -373,8 +377,8 @@ void setup_common(nimbleComm* c) {
     c->win_table.assign(static_cast<size_t>(kMaxWindows) * kMaxRanks, 0);
 }
 
+// Never throws; the caller has made c's device current.
 void free_regions(nimbleComm* c) {
-    DeviceGuard g(c->device);
     for (void* p : c->ipc_mapped) cudaIpcCloseMemHandle(p);
     c->ipc_mapped.clear();
     if (c->ctrl) cudaFree(c->ctrl);
@@ -1003,6 +1007,31 @@ nimbleResult_t nimbleCommInitAll(nimbleComm_t* comms, int ndev, const int* devli
     });
 }
 
+nimbleComm::~nimbleComm() {
+    // never throws: a comm whose init failed may have no usable device
+    int prev = -1;
+    if (cudaGetDevice(&prev) != cudaSuccess || cudaSetDevice(device) != cudaSuccess) {
+        cudaGetLastError();
+        prev = -1;
+    }
+    for (nb::Window& w : windows)
+        for (void* p : w.opened) nb::ipc_cache().release(p);
+    windows.clear();
+    schedules.clear();
+    fast.cs = last_cs = nullptr;
+    nb::free_regions(this);
+    cudaFree(d_view);
+    cudaFree(d_win_table);
+    cudaFree(d_scratch);
+    cudaFree(d_epoch);
+    if (d_trace) cudaFree(d_trace);
+    if (h_status) cudaFreeHost(h_status);
+    if (bench_stream) cudaStreamDestroy(bench_stream);
+    if (last_launch) cudaEventDestroy(last_launch);
+    cudaGetLastError();
+    if (prev >= 0) cudaSetDevice(prev);
+}
+
 nimbleResult_t nimbleCommDestroy(nimbleComm_t c) {
     if (!c) return nimbleSuccess;
     return guarded([&] {
@@ -1010,25 +1039,12 @@ nimbleResult_t nimbleCommDestroy(nimbleComm_t c) {
             nb::DeviceGuard g(c->device);
             cudaDeviceSynchronize();
             if (c->boot) c->boot->barrier();  // nobody touches my regions any more
-            for (nb::Window& w : c->windows)
-                for (void* p : w.opened) nb::ipc_cache().release(p);
-            c->schedules.clear();
-            c->fast.cs = c->last_cs = nullptr;
-            nb::free_regions(c);
-            cudaFree(c->d_view);
-            cudaFree(c->d_win_table);
-            cudaFree(c->d_scratch);
-            cudaFree(c->d_epoch);
-            if (c->d_trace) cudaFree(c->d_trace);
-            cudaFreeHost(c->h_status);
-            if (c->bench_stream) cudaStreamDestroy(c->bench_stream);
-            if (c->last_launch) cudaEventDestroy(c->last_launch);
         }
         if (c->clique) {
             auto& v = c->clique->comms;
             v.erase(std::remove(v.begin(), v.end(), c), v.end());
         }
-        delete c;
+        delete c;  // ~nimbleComm frees everything
     });
 }
 
@@ -1087,10 +1103,7 @@ nimbleResult_t nimbleCommSetConfig(nimbleComm_t c, const nimbleCommConfig* cfg) 
         if (regrow) {
             CUDA_TRY(cudaDeviceSynchronize());
             if (c->boot) c->boot->barrier();
-            for (void* p : c->ipc_mapped) cudaIpcCloseMemHandle(p);
-            c->ipc_mapped.clear();
-            cudaFree(c->staging);
-            cudaFree(c->ctrl);
+            nb::free_regions(c);  // nulls the pointers: a failing setup below leaves nothing to double-free
             c->cfg = next;
             nb::setup_regions(c, false);
             CUDA_TRY(cudaMemset(c->d_epoch, 0, sizeof(uint64_t)));  // fresh flags: epochs restart
