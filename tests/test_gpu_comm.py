@@ -285,7 +285,7 @@ def w_graph(comm, rank, R):
     return bads
 
 
-def w_overtake(comm, rank, R, big):
+def w_overtake(comm, rank, R, big, small):
     """Post slots are double-buffered by epoch parity.  A receiver that pulled
     everything it needed from a sender does not wait for that sender, so it
     can run two launches ahead and overwrite the post slot the sender has not
@@ -293,10 +293,11 @@ def w_overtake(comm, rank, R, big):
     waiting for a post that never comes back.  Here rank 1 is held in launch A
     by a `big` self copy whose items surround its small segment for rank 0.
     Rank 0 pulls that segment, runs launch B (its own self copy only), and
-    then launch C, whose post for rank 1 lands in A's slot."""
+    then launch C, whose post for rank 1 lands in A's slot.  With `small` under
+    the LL limit the same sequence exercises the LL slot reuse instead: rank 0's
+    launch C may write slot (A & 1) only once rank 1 acknowledged launch A."""
     from paper_2604_00317_b200 import comm as C
     comm.set_config(pull=2)  # every registered sender grants pulls
-    small = 4096 + 3
 
     def mat(a10, a11, a00):
         m = [0] * (R * R)
@@ -616,8 +617,9 @@ def test_comm_init_all_single_process_grouped():
 
 
 @need2
-def test_receiver_two_launches_ahead_of_sender():
-    out = _spawn("w_overtake", 2, 4 << 30)
+@pytest.mark.parametrize("small", [300 * 1024 + 3, 4096 + 3])  # pull path (> ll_max), LL path
+def test_receiver_two_launches_ahead_of_sender(small):
+    out = _spawn("w_overtake", 2, 4 << 30, small)
     assert all(v == 0 for v in out.values()), out
 
 
