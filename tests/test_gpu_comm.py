@@ -579,11 +579,12 @@ def test_comm_init_all_single_process_grouped():
     R = min(_ngpus(), 4)
     comms = C.Comm.init_all(list(range(R)))
     try:
-        for fabric, register in (("nvswitch", True), ("nvswitch", False), ("alltoall", True)):
+        for fabric, register, per_rank in (("nvswitch", True, 3 * MiB + 1), ("nvswitch", False, 3 * MiB + 1),
+                                           ("alltoall", True, 0), ("nvswitch", False, 100 * 1024 + 3)):  # last: LL
             for c in comms:
                 with torch.cuda.device(c.device):
                     c.set_config(fabric=fabric, gpus_per_node=R)
-            m = P.gen_p2p(R, 0, 1, 96 * MiB) if fabric == "alltoall" else P.gen_skewed_a2av(R, 3 * MiB + 1, 0.7, 0)
+            m = P.gen_p2p(R, 0, 1, 96 * MiB) if fabric == "alltoall" else P.gen_skewed_a2av(R, per_rank, 0.7, 0)
             bufs = []
             for c in comms:
                 with torch.cuda.device(c.device):
