@@ -482,6 +482,48 @@ def w_moe_autograd(comm, rank, R):
     return bool(ok), sum(h.recv_counts)
 
 
+def w_stress_ll(comm, rank, R):
+    """40 launches back to back without a host sync, alternating three small
+    skewed matrices whose pairs straddle the LL limit (some pairs LL, some on
+    the post / pull / push path) and two receive buffers each, then every
+    buffer's last delivery is verified."""
+    import random
+    from paper_2604_00317_b200 import comm as C
+    from paper_2604_00317_b200 import planner as P
+    rng = random.Random(11)  # same sequence on every rank
+    pool = []
+    for it, per_rank in enumerate((64 * 1024 + 5, 600 * 1024 + 1, 2 * MiB + 3)):
+        m = P.gen_skewed_a2av(R, per_rank, 0.7, it % R)
+        sc, sd, rc, rd = C.packed_displs(m, R, rank)
+        send = torch.empty(max(sum(sc), 16), dtype=torch.uint8, device="cuda")
+        for d in range(R):
+            C.fill_payload(send[sd[d]:], 0, sc[d], 70 + it, rank, d)
+        recvs = [torch.zeros(max(sum(rc), 16), dtype=torch.uint8, device="cuda") for _ in range(2)]
+        hs = [comm.register(send), comm.register(recvs[0])] if it != 1 else []
+        pool.append((sc, sd, rc, rd, send, recvs, hs, 70 + it))
+    torch.cuda.synchronize()
+    plan = [(rng.randrange(3), rng.randrange(2)) for _ in range(40)]
+    for k, (i, j) in enumerate(plan):
+        if k % 10 == 0:
+            comm.set_config(pull=rng.choice([0, 1, 2]))
+        sc, sd, rc, rd, send, recvs, hs, seed = pool[i]
+        comm.alltoallv(send, sc, sd, recvs[j], rc, rd)
+    torch.cuda.synchronize()
+    comm.check_async()
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for i, (sc, sd, rc, rd, send, recvs, hs, seed) in enumerate(pool):
+        for j in range(2):
+            if (i, j) in plan:
+                for s in range(R):
+                    C.check_payload(recvs[j][rd[s]:], 0, rc[s], seed, s, rank, bad)
+    torch.cuda.synchronize()
+    for (sc, sd, rc, rd, send, recvs, hs, seed) in pool:
+        for h in hs:
+            comm.deregister(h)
+    comm.set_config(pull=0)
+    return int(bad.item())
+
+
 def w_bench(comm, rank, R):
     return comm.bench_skewed(32 * MiB, 0.7, 0, warmup=1, iters=3)
 
@@ -649,3 +691,10 @@ def test_moe_custom_op_forward_and_gradients():
     R = min(_ngpus(), 4)
     res = _spawn("w_moe_autograd", R)
     assert all(ok for ok, _ in res.values()), res
+
+
+@need2
+def test_stress_ll_and_normal_pairs_back_to_back():
+    R = min(_ngpus(), 4)
+    out = _spawn("w_stress_ll", R)
+    assert all(v == 0 for v in out.values()), out
