@@ -62,3 +62,53 @@ def test_bootstrap_rejects_foreign_id(lib):
     u = _lib.UniqueId()
     out = (ctypes.c_uint64 * 2)()
     assert lib.nimbleBootstrapAllgather(ctypes.byref(u), 0, 1, out, 8, out) == 4
+
+
+def _worker_schedule(rank, world, port, q):
+    """Every rank plans and schedules on its own (as nimbleAlltoAllv does) and the
+    results are compared across processes: the replicated planner agrees, and
+    rank s's push ranges to d are exactly the ranges d pulls / drains from s."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2604_00317_b200 import planner as P
+    m = P.gen_irregular(world, 40 * (1 << 20) + 77, 0.8, 3)
+    topo = P.build_canonical(1, world, 0, 900e9, 0, P.NVSWITCH)
+    plan = P.plan_to_json(P.plan(topo, world, world, m))
+    plan["stats"].pop("wall_seconds")  # the only field that may differ: timing
+    pull_mask = 0b0101 & ((1 << world) - 1)
+    items = P.debug_schedule(topo, world, world, m, rank, staged_mask=0b0010, pull_mask=pull_mask,
+                             push_chunk=8192)
+    plans = [None] * world
+    scheds = [None] * world
+    dist.all_gather_object(plans, plan)
+    dist.all_gather_object(scheds, items)
+    ok = all(p == plans[0] for p in plans)
+    for s in range(world):
+        for d in range(world):
+            if s == d:
+                continue
+            push = sorted((it["dst"], it["bytes"]) for it in scheds[s] if it["kind"] == "push" and it["peer"] == d)
+            if (pull_mask >> s) & 1:  # receiver d asks s to let it pull: the pulls cover the pair
+                pulled = sum(it["bytes"] for it in scheds[d] if it["kind"] == "pull" and it["peer"] == s)
+                ok &= pulled == m[s * world + d]
+            if (0b0010 >> s) & 1:  # receiver d drains s's pushes through its self ring, same cut
+                fw = sorted((it["dst"], it["bytes"]) for it in scheds[d]
+                            if it["kind"] == "forward" and it["aux"] == s and it["peer"] == d)
+                ok &= fw == push
+            ok &= sum(b for _, b in push) == m[s * world + d]
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_replicated_planner_and_schedules_agree_across_processes(world):
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker_schedule, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
