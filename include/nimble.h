@@ -201,11 +201,11 @@ typedef struct {
                                      (8 KiB).  A port that pulls in while it pushes out runs
                                      both through one CTA ring; short pushes keep a store
                                      stalled on a busy egress from holding up the pulls   */
-    uint64_t ll_max;              /* direct pairs of at most ll_max bytes (<= 256 KiB) take the
+    uint64_t ll_max;              /* direct pairs of at most ll_max bytes (<= 1 MiB) take the
                                      low-latency protocol: the sender stores data with the
                                      epoch flag inline into the receiver's LL slot, and no
                                      posts, fences or completion handshake are needed.
-                                     Default 256 KiB; 0 disables                         */
+                                     Default 1 MiB; 0 disables                           */
 } nimbleCommConfig;
 
 nimbleResult_t nimbleCommConfigDefault(nimbleCommConfig* cfg);

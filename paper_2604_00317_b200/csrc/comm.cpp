@@ -1094,7 +1094,7 @@ nimbleResult_t nimbleCommSetConfig(nimbleComm_t c, const nimbleCommConfig* cfg) 
         nb::slot_count(next);
         nb::to_params(&next.planner);
         if (next.ll_max > nb::kLLMaxData)
-            throw nb::Error(nimbleInvalidArgument, "config: ll_max above the LL slot size (256 KiB)");
+            throw nb::Error(nimbleInvalidArgument, "config: ll_max above the LL slot size (1 MiB)");
         const bool regrow = next.pipe_chunk != c->cfg.pipe_chunk || next.p2p_buffer != c->cfg.p2p_buffer ||
                             next.channels_per_peer != c->cfg.channels_per_peer;
         nb::DeviceGuard g(c->device);

@@ -34,7 +34,7 @@ constexpr int kThreads = 512;  // forwarding-engine CTA size
 // and decodes -- no posts, no fences, no completion handshake.  Line 0 carries
 // the byte count.  Slots are double-buffered by epoch parity; a sender reuses
 // slot e & 1 only after the receiver acknowledged epoch e - 2 (ll_ack).
-constexpr uint64_t kLLMaxData = 256ull << 10;                               // bytes per pair
+constexpr uint64_t kLLMaxData = 1ull << 20;                                  // bytes per pair
 constexpr uint64_t kLLPiece = 8ull << 10;                                   // bytes per work item (one CTA)
 constexpr uint64_t kLLSlotBytes = ((1 + kLLMaxData / 8) * 16 + 255) / 256 * 256;  // header + lines
 

@@ -101,5 +101,5 @@ def test_comm_config_defaults_through_the_abi(lib):
     cfg = _lib.CommConfig()
     assert lib.nimbleCommConfigDefault(ctypes.byref(cfg)) == 0
     assert (cfg.fabric, cfg.pipe_chunk, cfg.p2p_buffer, cfg.channels_per_peer) == (1, 64 << 10, 10 << 20, 1)
-    assert (cfg.ctas, cfg.direct_chunk, cfg.pull, cfg.push_chunk, cfg.ll_max) == (0, 0, 0, 0, 256 << 10)
+    assert (cfg.ctas, cfg.direct_chunk, cfg.pull, cfg.push_chunk, cfg.ll_max) == (0, 0, 0, 0, 1 << 20)
     assert cfg.nvlink_bytes_per_s == 900e9

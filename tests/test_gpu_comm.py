@@ -331,18 +331,19 @@ def w_overtake(comm, rank, R, big, small):
 
 
 def w_ll(comm, rank, R):
-    """Low-latency protocol for pairs <= ll_max (256 KiB, cut into 8 KiB pieces):
+    """Low-latency protocol for pairs <= ll_max (1 MiB, cut into 8 KiB pieces):
     odd sizes around the piece and pair thresholds next to normal pairs, unaligned packed offsets, six back-to-back
     launches without a host sync (slot parity + acknowledgements), a CUDA graph
     replaying an all-LL exchange, and the same traffic with LL disabled."""
     from paper_2604_00317_b200 import comm as C
-    sizes = [1, 7, 8, 9, 8191, 8192, 8193, 40961, 65535, 65536, 65537, 262144, 262145, 1 << 20, 3]
+    sizes = [1, 7, 8, 9, 8191, 8192, 8193, 40961, 65535, 65536, 65537, 262144, 262145, 1 << 20, (1 << 20) + 1,
+             3 << 20, 3]
 
     def mat(shift):
         return [0 if s == d else sizes[(3 * s + 5 * d + shift) % len(sizes)] for s in range(R) for d in range(R)]
 
     out = []
-    for ll_max in (256 << 10, 64 << 10, 0):
+    for ll_max in (1 << 20, 256 << 10, 0):
         comm.set_config(ll_max=ll_max)
         runs = []
         for i in range(6):
@@ -366,7 +367,7 @@ def w_ll(comm, rank, R):
                 bad += int((recv[sum(rc):] != 0xEE).sum())
         torch.cuda.synchronize()
         out.append(int(bad.item()))
-    comm.set_config(ll_max=64 << 10)
+    comm.set_config(ll_max=1 << 20)
     # an all-LL exchange captured in a CUDA graph
     m = [0 if s == d else 1000 + 13 * s + d for s in range(R) for d in range(R)]
     sc, sd, rc, rd = C.packed_displs(m, R, rank)
@@ -417,7 +418,7 @@ def w_sendrecv_mixed(comm, rank, R):
     right, left = (rank + 1) % R, (rank - 1) % R
     bad = torch.zeros(1, dtype=torch.int64, device="cuda")
     if R == 2:  # one peer: an LL-sized message one way, a normal-path one back
-        for it, (small, big) in enumerate([(3, 300001), (262144, 262145)]):
+        for it, (small, big) in enumerate([(3, (1 << 20) + 300001), (262144, 3 * MiB + 1)]):
             n_out, n_in = (small, big) if rank == 0 else (big, small)
             x = torch.empty(n_out, dtype=torch.uint8, device="cuda")
             C.fill_payload(x, 0, n_out, 500 + it, rank, 1 - rank)
@@ -660,7 +661,7 @@ def test_comm_init_all_single_process_grouped():
 
 
 @need2
-@pytest.mark.parametrize("small", [300 * 1024 + 3, 4096 + 3])  # pull path (> ll_max), LL path
+@pytest.mark.parametrize("small", [(1 << 20) + 300 * 1024 + 3, 4096 + 3])  # pull path (> ll_max), LL path
 def test_receiver_two_launches_ahead_of_sender(small):
     out = _spawn("w_overtake", 2, 4 << 30, small)
     assert all(v == 0 for v in out.values()), out
@@ -670,7 +671,7 @@ def test_receiver_two_launches_ahead_of_sender(small):
 def test_low_latency_protocol_small_pairs():
     R = min(_ngpus(), 4)
     out = _spawn("w_ll", R)
-    assert all(v == [0, 0, 0, 0] for v in out.values()), out
+    assert all(v == [0, 0, 0, 0] for v in out.values()), out  # three ll_max settings + the graph
 
 
 @need2
