@@ -15,6 +15,20 @@ from ._lib import c_double, c_int, c_size, c_u64, c_void_p
 UINT8 = 1  # nimbleUint8
 
 
+def _load_fast():
+    """The CPython fast call into nimbleAlltoAllv (csrc/pyfast.cpp), bound to the
+    function of the library _lib loaded; None if the module was not built."""
+    try:
+        from . import _fast
+    except ImportError:
+        return None
+    _fast.init(ctypes.cast(_lib.lib().nimbleAlltoAllv, c_void_p).value)
+    return _fast
+
+
+_FAST = _load_fast()
+
+
 def _ptr(t) -> int:
     return t.data_ptr() if hasattr(t, "data_ptr") else int(t)
 
@@ -61,6 +75,7 @@ class Comm:
 
     def __init__(self, handle):
         self._h = c_void_p(handle) if not isinstance(handle, c_void_p) else handle
+        self._hv = self._h.value  # plain int for the fast call
         n, r, d = c_int(), c_int(), c_int()
         _lib.call("nimbleCommCount", self._h, ctypes.byref(n))
         _lib.call("nimbleCommUserRank", self._h, ctypes.byref(r))
@@ -87,6 +102,7 @@ class Comm:
         if self._h:
             _lib.call("nimbleCommDestroy", self._h)
             self._h = None
+            self._hv = 0
 
     @property
     def handle(self):
@@ -134,9 +150,14 @@ class Comm:
 
     # -- data path (counts / displacements in bytes: uint8 datatype)
     def alltoallv(self, send, sendcounts, sdispls, recv, recvcounts, rdispls, stream=None, datatype=UINT8):
-        fn = _lib.lib().nimbleAlltoAllv  # argtypes convert plain ints to pointers
-        _lib.check(fn(_ptr(send), _sizes(sendcounts), _sizes(sdispls), _ptr(recv), _sizes(recvcounts),
-                      _sizes(rdispls), datatype, self._h, _stream_handle(stream)))
+        if _FAST is not None:  # same C entry point, without ctypes' per-call conversions
+            rc = _FAST.alltoallv(self._hv, _ptr(send), sendcounts, sdispls, _ptr(recv), recvcounts, rdispls,
+                                 datatype, _stream_handle(stream))
+        else:
+            rc = _lib.lib().nimbleAlltoAllv(_ptr(send), _sizes(sendcounts), _sizes(sdispls), _ptr(recv),
+                                            _sizes(recvcounts), _sizes(rdispls), datatype, self._h,
+                                            _stream_handle(stream))
+        _lib.check(rc)
 
     def alltoall(self, send, recv, count, stream=None, datatype=UINT8):
         _lib.call("nimbleAlltoAll", c_void_p(_ptr(send)), c_void_p(_ptr(recv)), count, datatype, self._h,

@@ -103,3 +103,17 @@ def test_comm_config_defaults_through_the_abi(lib):
     assert (cfg.fabric, cfg.pipe_chunk, cfg.p2p_buffer, cfg.channels_per_peer) == (1, 64 << 10, 10 << 20, 1)
     assert (cfg.ctas, cfg.direct_chunk, cfg.pull, cfg.push_chunk, cfg.ll_max) == (0, 0, 0, 0, 1 << 20)
     assert cfg.nvlink_bytes_per_s == 900e9
+
+
+def test_python_fast_call_binds_the_same_entry_point(lib):
+    """comm.py's CPython fast call (csrc/pyfast.cpp) reaches nimbleAlltoAllv of the
+    library _lib loaded and reports its result codes; bad arguments raise."""
+    import pytest
+    from paper_2604_00317_b200 import comm as C
+    assert C._FAST is not None, "the _fast module was not built"
+    rc = C._FAST.alltoallv(0, 0, [1, 2], [0, 1], 0, [1, 2], [0, 1], 1, 0)  # null comm
+    assert rc == 4 and b"null argument" in lib.nimbleGetLastError()
+    with pytest.raises(ValueError):
+        C._FAST.alltoallv(0, 0, [1, 2], [0], 0, [1, 2], [0, 1], 1, 0)
+    with pytest.raises(TypeError):
+        C._FAST.alltoallv(0, 0, [1, 2], [0, 1], 0, [1, 2], [0, 1], 1)
