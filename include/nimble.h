@@ -189,15 +189,16 @@ typedef struct {
                                      slots = channels * p2p_buffer / pipe_chunk <= 256  */
     int channels_per_peer;        /* rings per relayed flow, 1 (pipeline.hpp:23)        */
     int ctas;                     /* forwarding-engine CTAs per launch, 0 = auto        */
-    uint64_t direct_chunk;        /* work-item size of direct pulls, self rings and local
-                                     copies (<= pipe_chunk), 0 = auto (128 KiB, capped at
-                                     pipe_chunk)                                           */
+    uint64_t direct_chunk;        /* work-item size of direct pulls and local copies
+                                     (<= pipe_chunk), 0 = auto (128 KiB, capped at
+                                     pipe_chunk = 64 KiB)                                  */
     int pull;                     /* receiver-driven pulls.  0 = auto (default): receivers
                                      ask; a registered sender grants unless its own port is
                                      ingress-bound (ingress > 1.2 x egress; 1.55 x with two
                                      ranks), in which case it pushes out; 1 = never (push
                                      only); 2 = always grant                             */
-    uint64_t push_chunk;          /* work-item size of direct pushes (<= pipe_chunk), 0 = auto
+    uint64_t push_chunk;          /* work-item size of direct pushes and of the staged self
+                                     rings that mirror them (<= pipe_chunk), 0 = auto
                                      (8 KiB).  A port that pulls in while it pushes out runs
                                      both through one CTA ring; short pushes keep a store
                                      stalled on a busy egress from holding up the pulls   */
