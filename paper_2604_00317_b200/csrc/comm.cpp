@@ -407,7 +407,13 @@ std::shared_ptr<PlanResult> plan_for(nimbleComm* c, const std::vector<uint64_t>&
     Demand d;
     d.ranks = c->nranks;
     d.bytes = matrix;
-    auto p = std::make_shared<PlanResult>(mcf_plan(lm, c->nranks, lm.gpus, d, to_params(&c->cfg.planner)));
+    // On the nvswitch model every pair has exactly one candidate (direct), so
+    // the MCF sweep can only put each pair's demand on it: the direct plan has
+    // the same flows (tests/test_planner_parity.py) at a fraction of the cost
+    // -- it matters when every call brings a new matrix (MoE dispatch).
+    auto p = std::make_shared<PlanResult>(c->cfg.fabric == nimbleFabricNvSwitch
+                                              ? direct_plan(lm, c->nranks, lm.gpus, d)
+                                              : mcf_plan(lm, c->nranks, lm.gpus, d, to_params(&c->cfg.planner)));
     c->plans.push_front({key, p, ++c->plan_ids, p->stats.wall_seconds});
     if (c->plans.size() > 4) c->plans.pop_back();
     *plan_id = c->plan_ids;

@@ -264,3 +264,19 @@ def test_plan_from_reference_json(lib):
         back = P.plan_from_json(t, req["ranks"], _cases.rpn(req), resp["plan"])
         assert [pp.flows for pp in back.pairs] == [[(c, b) for c, b in f] for f in _cases.ref_flows(resp)]
         assert back.link_loads == resp["loads"]
+
+
+def test_nvswitch_mcf_plan_equals_direct_plan_flows(lib):
+    """The communicator plans nvswitch exchanges with the direct plan (comm.cpp
+    plan_for): with one candidate per pair the MCF sweep has no choice, so its
+    flows must equal the direct plan's on any matrix."""
+    import random
+    rng = random.Random(5)
+    for R in (2, 3, 4, 8):
+        topo = P.build_canonical(1, R, 0, 900e9, 0, P.NVSWITCH)
+        for _ in range(100):
+            m = [0 if i // R == i % R else rng.choice([0, rng.randint(1, 1 << 30), rng.randint(1, 1 << 20)])
+                 for i in range(R * R)]
+            a = P.plan(topo, R, R, m)
+            b = P.plan_direct_baseline(topo, R, R, m)
+            assert [(p.src, p.dst, p.flows) for p in a.pairs] == [(p.src, p.dst, p.flows) for p in b.pairs]
