@@ -118,6 +118,9 @@ class Refiner {
     }
 
     std::uint64_t run() {
+        bool choice = false;  // with one route per pair no move exists (e.g. the nvswitch model)
+        for (const PairRoutes& pr : pairs_) choice |= pr.cands.size() > 1;
+        if (!choice) return 0;
         for (int round = 0; round < 8; ++round) {
             const bool r = reduce();
             const bool c = consolidate();
@@ -347,6 +350,19 @@ PlanResult mcf_plan(const LinkModel& lm, int ranks, int rpn, const Demand& m, co
             const PairRoutes& pr = res.pairs[i];
             double r = left[i];
             double budget = r < eps ? r : std::max(eps, std::floor(r * p.lambda / eps) * eps);
+            if (pr.cands.size() == 1 && budget > 0.0) {
+                // One route: every chunk of the visit lands on it.  Loads are
+                // integer-valued doubles below 2^53, so adding the visit at once
+                // leaves the same loads, flows and counts as chunk by chunk.
+                const double full = std::floor(budget / eps);
+                const bool tail = budget - full * eps > 0.0;
+                book.add_route(pr.cands[0], budget);
+                acc[i][0] += budget;
+                res.stats.placements += static_cast<std::uint64_t>(full) + (tail ? 1 : 0);
+                if (tail) ++res.stats.residual_flows;
+                r -= budget;
+                budget = 0.0;
+            }
             while (budget > 0.0) {
                 const double chunk = std::min(eps, budget);
                 size_t best = 0;
