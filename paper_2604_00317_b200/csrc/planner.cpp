@@ -49,10 +49,21 @@ void intra(const LinkModel& lm, int node, int a, int b, Candidate& c) {
 struct LoadBook {
     const LinkModel& lm;
     std::vector<double> load, drain;
+    // Links whose drain is >= bar, kept current by add(): "peak() < bar" is
+    // then "nhot == 0" in O(1) -- the refiner's trial moves touch <= 4 links.
+    double bar = std::numeric_limits<double>::infinity();
+    int nhot = 0;
     explicit LoadBook(const LinkModel& m) : lm(m), load(m.cap.size(), 0.0), drain(m.cap.size(), 0.0) {}
     void add(int e, double x) {
+        const bool was = drain[e] >= bar;
         load[e] += x;
         drain[e] = load[e] / lm.cap[e];
+        nhot += static_cast<int>(drain[e] >= bar) - static_cast<int>(was);
+    }
+    void set_bar(double b) {
+        bar = b;
+        nhot = 0;
+        for (double v : drain) nhot += v >= b;
     }
     void add_route(const Candidate& c, double x) {
         for (int k = 0; k < c.ne; ++k) add(c.e[k], x);
@@ -70,6 +81,7 @@ struct LoadBook {
     void reset(const std::vector<double>& l) {
         load = l;
         for (size_t e = 0; e < load.size(); ++e) drain[e] = load[e] / lm.cap[e];
+        set_bar(bar);
     }
 };
 
@@ -157,6 +169,7 @@ class Refiner {
             const double cur = book_.peak();
             if (cur <= 0.0) break;
             const double bar = cur * (1.0 - 1e-12);
+            book_.set_bar(bar);
             for (size_t i = 0; i < pairs_.size() && !progress; ++i) {
                 const auto& cs = pairs_[i].cands;
                 for (size_t c = 0; c < cs.size() && !progress; ++c) {
@@ -166,7 +179,7 @@ class Refiner {
                     for (size_t a = 0; a < cs.size(); ++a) {
                         if (a == c || pen(i, a) > pc) continue;
                         move(i, c, a, q);
-                        if (book_.peak() < bar) {
+                        if (book_.nhot == 0) {  // peak() < bar
                             ++moves_;
                             progress = any = true;
                             break;
@@ -214,6 +227,7 @@ class Refiner {
         const double cur = book_.peak();
         if (cur <= 0.0) return false;
         const double bar = cur * (1.0 - 1e-12);
+        book_.set_bar(bar);
         for (size_t i = 0; i < pairs_.size(); ++i) {
             const auto& cs = pairs_[i].cands;
             for (size_t c = 0; c < cs.size(); ++c) {
@@ -226,7 +240,7 @@ class Refiner {
                     for (int k = 0; k < cs[a].ne; ++k) {
                         const int hot = cs[a].e[k];
                         if (book_.drain[hot] < bar) continue;
-                        if (evict_from(hot, i, a, c, bar)) return true;
+                        if (evict_from(hot, i, a, c)) return true;
                     }
                     move(i, a, c, q);
                     if (ejects_ >= kEjectCap) return false;
@@ -238,7 +252,7 @@ class Refiner {
 
     // Try to move one chunk of some other route that crosses link `hot` to a
     // sibling route of its own pair, so the peak drops below `bar`.
-    bool evict_from(int hot, size_t i, size_t a, size_t c, double bar) {
+    bool evict_from(int hot, size_t i, size_t a, size_t c) {  // the book's bar is eject()'s
         for (size_t j = 0; j < pairs_.size(); ++j) {
             const auto& js = pairs_[j].cands;
             for (size_t d = 0; d < js.size(); ++d) {
@@ -252,7 +266,7 @@ class Refiner {
                     if (ejects_ >= kEjectCap) break;
                     ++ejects_;
                     move(j, d, b, v);
-                    if (book_.peak() < bar) {
+                    if (book_.nhot == 0) {  // peak() < bar (set_bar in eject)
                         moves_ += 2;
                         return true;
                     }
