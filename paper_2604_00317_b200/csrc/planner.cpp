@@ -85,16 +85,23 @@ struct LoadBook {
     }
 };
 
-double route_cost(const Candidate& c, const LoadBook& book, const CostParams& cost,
-                  std::uint64_t message, double pending) {
+// max over the route's links of the (normalized) load after adding `pending`
+double route_load_cost(const Candidate& c, const LoadBook& book, const CostParams& cost, double pending) {
     double worst = 0.0;
     for (int k = 0; k < c.ne; ++k) {
         const int e = c.e[k];
         const double v = cost.normalize ? (book.load[e] + pending) / book.lm.cap[e] : book.load[e] + pending;
         worst = std::max(worst, v);
     }
-    return worst + cost.penalty(c, message);
+    return worst;
 }
+
+double route_cost(const Candidate& c, const LoadBook& book, const CostParams& cost,
+                  std::uint64_t message, double pending) {
+    return route_load_cost(c, book, cost, pending) + cost.penalty(c, message);
+}
+
+constexpr size_t kMaxCands = 64;  // routes per pair whose penalties the sweep caches
 
 std::vector<PairRoutes> active_pairs(const LinkModel& lm, int ranks, int rpn, const Demand& m) {
     m.check();
@@ -377,12 +384,18 @@ PlanResult mcf_plan(const LinkModel& lm, int ranks, int rpn, const Demand& m, co
                 r -= budget;
                 budget = 0.0;
             }
+            // the hop penalty depends on the route and the pair's demand only
+            double pens[kMaxCands];
+            const size_t nc = std::min(pr.cands.size(), kMaxCands);
+            if (budget > 0.0)
+                for (size_t c = 0; c < nc; ++c) pens[c] = p.cost.penalty(pr.cands[c], pr.demand);
             while (budget > 0.0) {
                 const double chunk = std::min(eps, budget);
                 size_t best = 0;
                 double best_cost = std::numeric_limits<double>::infinity();
                 for (size_t c = 0; c < pr.cands.size(); ++c) {
-                    const double cost = route_cost(pr.cands[c], book, p.cost, pr.demand, chunk);
+                    const double cost = c < nc ? route_load_cost(pr.cands[c], book, p.cost, chunk) + pens[c]
+                                               : route_cost(pr.cands[c], book, p.cost, pr.demand, chunk);
                     if (cost < best_cost) {
                         best_cost = cost;
                         best = c;
