@@ -10,62 +10,81 @@ namespace nb {
 
 namespace {
 
-struct Keyed {
-    double key;
-    uint64_t flow_bytes;
-    uint32_t order;  // insertion order: deterministic tie break
-    Item item;
+// One flow's items, generated when they are merged: item k covers bytes
+// [k * chunk, min((k + 1) * chunk, bytes)) and sorts by the key
+// (k + 0.5) / n + phase -- its progress fraction.
+struct FlowCut {
+    Item proto;
+    uint64_t src0, dst0, bytes, chunk, n;
+    double phase;
+    uint32_t base;          // insertion order of item 0: the deterministic tie break
+    bool pull;              // pulls: src = dst - src_from_dst (offset inside the sender's segment)
+    uint64_t src_from_dst;
 };
 
-void cut(std::vector<Keyed>& out, Item proto, uint64_t src0, uint64_t dst0, uint64_t bytes, uint64_t chunk,
-         double phase) {
+struct Cuts {
+    std::vector<FlowCut> flows;
+    uint32_t count = 0;  // items so far
+};
+
+// Appends one flow; returns its item count.
+uint32_t cut(Cuts& out, Item proto, uint64_t src0, uint64_t dst0, uint64_t bytes, uint64_t chunk, double phase,
+             bool pull = false, uint64_t src_from_dst = 0) {
     const uint64_t n = (bytes + chunk - 1) / chunk;
-    for (uint64_t k = 0; k < n; ++k) {
-        Item it = proto;
-        const uint64_t off = k * chunk;
-        it.src = src0 ? src0 + off : 0;
-        it.dst = dst0 + off;
-        it.bytes = static_cast<uint32_t>(std::min(chunk, bytes - off));
-        it.seq = static_cast<uint32_t>(k);
-        out.push_back({(static_cast<double>(k) + 0.5) / static_cast<double>(n) + phase, bytes,
-                       static_cast<uint32_t>(out.size()), it});
-    }
+    if (n) out.flows.push_back({proto, src0, dst0, bytes, chunk, n, phase, out.count, pull, src_from_dst});
+    out.count += static_cast<uint32_t>(n);
+    return static_cast<uint32_t>(n);
 }
 
-bool before(const Keyed& a, const Keyed& b) {
+Item item_of(const FlowCut& f, uint64_t k) {
+    Item it = f.proto;
+    const uint64_t off = k * f.chunk;
+    it.src = f.src0 ? f.src0 + off : 0;
+    it.dst = f.dst0 + off;
+    it.bytes = static_cast<uint32_t>(std::min(f.chunk, f.bytes - off));
+    it.seq = static_cast<uint32_t>(k);
+    if (f.pull) it.src = it.dst - f.src_from_dst;
+    return it;
+}
+
+struct Cursor {
+    double key;
+    const FlowCut* f;
+    uint64_t k;
+};
+
+double key_of(const FlowCut& f, uint64_t k) {
+    return (static_cast<double>(k) + 0.5) / static_cast<double>(f.n) + f.phase;
+}
+
+// Strict, total order: key, then hot (larger) flows first on ties, then insertion order.
+bool before(const Cursor& a, const Cursor& b) {
     if (a.key != b.key) return a.key < b.key;
-    if (a.flow_bytes != b.flow_bytes) return a.flow_bytes > b.flow_bytes;  // hot flows first on ties
-    return a.order < b.order;
+    if (a.f->bytes != b.f->bytes) return a.f->bytes > b.f->bytes;
+    return a.f->base + a.k < b.f->base + b.k;
 }
 
-// The items in `before` order.  Every cut() appends one flow's items with
-// increasing keys, so v is a few dozen sorted runs: a k-way merge gives the
-// same total order as sorting (before() is strict and total -- `order` is
-// unique) in O(n log runs), which matters when every call brings a new matrix
-// (40-50k items at 256 MiB per rank).
-std::vector<Item> ordered(std::vector<Keyed>& v) {
-    std::vector<std::pair<size_t, size_t>> runs;  // [begin, end) of maximal sorted runs
-    for (size_t i = 0; i < v.size();) {
-        size_t j = i + 1;
-        while (j < v.size() && before(v[j - 1], v[j])) ++j;
-        runs.push_back({i, j});
-        i = j;
-    }
+// All items in `before` order: a k-way merge over the flows (each one's keys
+// increase with k), generating items as they are emitted -- O(n log flows)
+// with no per-item sort records, which matters when every call brings a new
+// matrix (35-53k items at 256 MiB per rank).
+std::vector<Item> ordered(const Cuts& cuts) {
+    std::vector<Cursor> heap;
+    heap.reserve(cuts.flows.size());
+    for (const FlowCut& f : cuts.flows) heap.push_back({key_of(f, 0), &f, 0});
+    auto later = [](const Cursor& a, const Cursor& b) { return before(b, a); };  // min-heap
+    std::make_heap(heap.begin(), heap.end(), later);
     std::vector<Item> items;
-    items.reserve(v.size());
-    // min-heap of run heads (std heap is a max-heap: invert the comparison)
-    auto later = [&](const std::pair<size_t, size_t>& a, const std::pair<size_t, size_t>& b) {
-        return before(v[b.first], v[a.first]);
-    };
-    std::make_heap(runs.begin(), runs.end(), later);
-    while (!runs.empty()) {
-        std::pop_heap(runs.begin(), runs.end(), later);
-        std::pair<size_t, size_t>& r = runs.back();
-        items.push_back(v[r.first].item);
-        if (++r.first == r.second) {
-            runs.pop_back();
+    items.reserve(cuts.count);
+    while (!heap.empty()) {
+        std::pop_heap(heap.begin(), heap.end(), later);
+        Cursor& c = heap.back();
+        items.push_back(item_of(*c.f, c.k));
+        if (++c.k == c.f->n) {
+            heap.pop_back();
         } else {
-            std::push_heap(runs.begin(), runs.end(), later);
+            c.key = key_of(*c.f, c.k);
+            std::push_heap(heap.begin(), heap.end(), later);
         }
     }
     return items;
@@ -97,7 +116,7 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
     Schedule sc;
     sc.posts = rb.recv_post;
     sc.send_posts = rb.send_post;
-    std::vector<Keyed> keyed;
+    Cuts keyed;
 
     // self segment: local copy
     if (rb.send_bytes[me] != rb.recv_bytes[me])
@@ -161,9 +180,7 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
                     Item proto{};
                     proto.kind = kPush;
                     proto.peer = static_cast<uint8_t>(d);
-                    const size_t first = keyed.size();
-                    cut(keyed, proto, rb.send_ptr[d] + off, off, bytes, schunk, 0.0);
-                    sc.push_items[d] += static_cast<uint32_t>(keyed.size() - first);
+                    sc.push_items[d] += cut(keyed, proto, rb.send_ptr[d] + off, off, bytes, schunk, 0.0);
                     sc.push_targets |= 1ull << d;
                     sc.write_targets |= 1ull << d;
                     sc.moved_bytes += bytes;
@@ -175,11 +192,9 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
                         Item proto{};
                         proto.kind = kPull;
                         proto.peer = static_cast<uint8_t>(s);
-                        const size_t first = keyed.size();
-                        cut(keyed, proto, 0, rb.recv_ptr[s] + off, bytes, dchunk, 0.0);
-                        for (size_t i = first; i < keyed.size(); ++i)  // source: offset inside the sender's segment
-                            keyed[i].item.src = keyed[i].item.dst - rb.recv_ptr[s];
-                        sc.pull_items[s] += static_cast<uint32_t>(keyed.size() - first);
+                        // source: offset inside the sender's segment
+                        sc.pull_items[s] += cut(keyed, proto, 0, rb.recv_ptr[s] + off, bytes, dchunk, 0.0, true,
+                                              rb.recv_ptr[s]);
                     }
                     if ((rb.recv_post[s].mode & 0xf) == kPostStaged) {  // drain my self ring (s, me)
                         Item proto{};
@@ -215,9 +230,7 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
                     proto.kind = kForward;
                     proto.peer = static_cast<uint8_t>(d);
                     proto.aux = static_cast<uint16_t>(s);
-                    const size_t first = keyed.size();
-                    cut(keyed, proto, 0, off, bytes, pipe_chunk, kHop2);
-                    sc.fwd_items[d] += static_cast<uint32_t>(keyed.size() - first);
+                    sc.fwd_items[d] += cut(keyed, proto, 0, off, bytes, pipe_chunk, kHop2);
                     sc.write_targets |= 1ull << d;
                 }
                 if (d == me) sc.relay_writers |= 1ull << v;
@@ -234,7 +247,7 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
 
 std::vector<Item> build_local_items(int R, const uint64_t* m, const uint64_t* send_base, const uint64_t* recv_base,
                                     uint64_t chunk) {
-    std::vector<Keyed> keyed;
+    Cuts keyed;
     for (int s = 0; s < R; ++s) {
         uint64_t soff = 0;
         for (int d = 0; d < R; ++d) {
