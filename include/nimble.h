@@ -325,6 +325,27 @@ nimbleResult_t nimbleDebugSchedule(nimblePlan_t plan, int rank, int ranks, uint6
  * at comm creation; n >= 16. */
 nimbleResult_t nimbleCommDebugTrace(nimbleComm_t comm, uint64_t* out, int n);
 
+/* Device counters of the forwarding engine, accumulated over the comm's
+ * launches (NIMBLE_STATS=1 at comm creation, on every rank).  bytes/items are
+ * indexed [kind][peer]: kind 0 local copy, 1 push (by receiver), 2 stage into
+ * a relay's ring (by relay), 3 forward out of a ring hosted here (by final
+ * receiver), 4 pull (by sender), 5 LL send (by receiver), 6 LL receive (by
+ * sender), 7 drain of my own staged-receive ring (by sender).  The slot
+ * counters check the bounded-buffer invariant of the staging rings on the
+ * device (proj/tests/acceptance.cpp:270-288, occupancy <= S): the largest
+ * number of claimed-not-drained slots any of my stager claims observed in its
+ * ring, and the number of claims of a slot whose previous chunk had not been
+ * drained (must be 0).  reset != 0 zeroes the counters after reading. */
+typedef struct {
+    uint64_t bytes[8][32];
+    uint64_t items[8][32];
+    uint64_t slot_max_occupancy;
+    uint64_t slot_double_claims;
+    uint64_t slot_claims;
+    uint64_t pad;
+} nimbleCommStats;
+nimbleResult_t nimbleCommGetStats(nimbleComm_t comm, nimbleCommStats* stats, int reset);
+
 #ifdef __cplusplus
 }
 #endif

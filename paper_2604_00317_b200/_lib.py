@@ -58,6 +58,11 @@ class BenchResult(ctypes.Structure):  # nimbleBenchResult
                 ("mismatches", c_u64), ("relay_flows", c_int)]
 
 
+class CommStats(ctypes.Structure):  # nimbleCommStats
+    _fields_ = [("bytes", (c_u64 * 32) * 8), ("items", (c_u64 * 32) * 8), ("slot_max_occupancy", c_u64),
+                ("slot_double_claims", c_u64), ("slot_claims", c_u64), ("pad", c_u64)]
+
+
 # name -> argtypes (restype is always nimbleResult_t unless listed in _RESTYPES)
 SIGNATURES = {
     "nimbleGetErrorString": [c_int],
@@ -123,6 +128,7 @@ SIGNATURES = {
     "nimbleBenchMatrix": [c_void_p, P(c_u64), c_int, c_int, P(BenchResult)],
     "nimbleBootstrapAllgather": [P(UniqueId), c_int, c_int, c_void_p, c_size, c_void_p],
     "nimbleCommDebugTrace": [c_void_p, P(c_u64), c_int],
+    "nimbleCommGetStats": [c_void_p, P(CommStats), c_int],
     "nimbleDebugSchedule": [c_void_p, c_int, c_int, c_u64, ctypes.c_uint32, c_u64, c_u64, c_u64, c_u64, c_void_p, c_int,
                             P(c_int)],
 }

@@ -138,6 +138,21 @@ class Comm:
         _lib.call("nimbleCommDebugTrace", self._h, out, 16)
         return list(out)
 
+    STAT_KINDS = ("local", "push", "stage", "forward", "pull", "ll_send", "ll_recv", "drain")
+
+    def stats(self, reset=False) -> dict:
+        """Engine counters since creation / the last reset (needs NIMBLE_STATS=1
+        when the comm was created): bytes and items per (kind, peer) and the
+        staging rings' slot-occupancy check (include/nimble.h)."""
+        st = _lib.CommStats()
+        _lib.call("nimbleCommGetStats", self._h, ctypes.byref(st), 1 if reset else 0)
+        out = {"slot_max_occupancy": st.slot_max_occupancy, "slot_double_claims": st.slot_double_claims,
+               "slot_claims": st.slot_claims}
+        for k, name in enumerate(self.STAT_KINDS):
+            out[name] = [int(st.bytes[k][p]) for p in range(self.nranks)]
+            out[name + "_items"] = [int(st.items[k][p]) for p in range(self.nranks)]
+        return out
+
     # -- registration
     def register(self, tensor, nbytes=None):
         h = c_void_p()
@@ -150,6 +165,9 @@ class Comm:
 
     # -- data path (counts / displacements in bytes: uint8 datatype)
     def alltoallv(self, send, sendcounts, sdispls, recv, recvcounts, rdispls, stream=None, datatype=UINT8):
+        n = self.nranks
+        if len(sendcounts) != n or len(sdispls) != n or len(recvcounts) != n or len(rdispls) != n:
+            raise ValueError(f"alltoallv: counts and displacements need exactly {n} entries (one per rank)")
         if _FAST is not None:  # same C entry point, without ctypes' per-call conversions
             rc = _FAST.alltoallv(self._hv, _ptr(send), sendcounts, sdispls, _ptr(recv), recvcounts, rdispls,
                                  datatype, _stream_handle(stream))

@@ -15,6 +15,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -128,17 +129,22 @@ struct DevBuf {
         return *this;
     }
     ~DevBuf() { release(); }
+    // Stream-ordered (de)allocation: cudaFree would synchronize the whole
+    // device, and on a device hosting several ranks of one comm that means
+    // waiting for a peer's engine grid that may itself wait for this rank's
+    // next launch.  The buffer is idle whenever it grows or is released (the
+    // schedule cache waits for the entry's last launch first).
     void assign(const std::vector<T>& v, cudaStream_t st) {
         if (v.size() > n) {
-            if (p) cudaFree(p);
+            if (p) CUDA_TRY(cudaFreeAsync(p, st));
             p = nullptr;
-            CUDA_TRY(cudaMalloc(&p, std::max<size_t>(v.size(), 1) * sizeof(T)));
+            CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(v.size(), 1) * sizeof(T), st));
             n = v.size();
         }
         if (!v.empty()) CUDA_TRY(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, cudaStreamPerThread);
         p = nullptr;
         n = 0;
     }
@@ -148,6 +154,7 @@ struct PeerInfo {
     int32_t pid;
     int32_t dev;
     uint64_t host;
+    uint64_t ctrl_ptr, staging_ptr;  // raw pointers: a peer in this process maps nothing
     cudaIpcMemHandle_t ctrl, staging;
 };
 
@@ -164,6 +171,13 @@ struct CachedPlan {
     double seconds = 0;
 };
 
+// Pin count of a schedule captured into CUDA graphs: shared with the graphs'
+// user objects, whose destructors (CUDA-internal threads, no CUDA calls
+// allowed) only decrement it.
+struct GraphPins {
+    std::atomic<int> n{0};
+};
+
 struct CachedSchedule {
     std::vector<uint64_t> key;
     Schedule sc;
@@ -172,6 +186,24 @@ struct CachedSchedule {
     DevBuf<Post> send_posts;
     DevBuf<uint64_t> finals;
     DevBuf<Item> ll_items;
+    cudaEvent_t used = nullptr;  // recorded after every eager launch of this entry
+    std::shared_ptr<GraphPins> pins = std::make_shared<GraphPins>();
+    CachedSchedule() = default;
+    CachedSchedule(const CachedSchedule&) = delete;
+    CachedSchedule(CachedSchedule&& o) noexcept
+        : key(std::move(o.key)), sc(std::move(o.sc)), items(std::move(o.items)), posts(std::move(o.posts)),
+          send_posts(std::move(o.send_posts)), finals(std::move(o.finals)), ll_items(std::move(o.ll_items)),
+          used(o.used), pins(std::move(o.pins)) {
+        o.used = nullptr;
+    }
+    ~CachedSchedule() {
+        if (used) cudaEventDestroy(used);
+    }
+    bool pinned() const { return pins && pins->n.load() > 0; }
+    // no launch of this comm still reads the entry's device buffers
+    void wait_idle() const {
+        if (used) cudaEventSynchronize(used);
+    }
 };
 
 struct Clique;
@@ -217,6 +249,10 @@ IpcCache& ipc_cache() {
 
 struct nimbleComm {
     int rank = 0, nranks = 1, device = 0, sms = 148;
+    // ranks of this comm on my device (one process, several streams): their
+    // engine grids must all be resident at once, so each launch takes at most
+    // sms_share CTAs by default
+    int colocated = 1, sms_share = 148;
     std::unique_ptr<nb::Bootstrap> boot;
     std::shared_ptr<nb::Clique> clique;
     nimbleCommConfig cfg{};
@@ -237,6 +273,7 @@ struct nimbleComm {
     uint64_t plan_ids = 0;
     std::list<nb::CachedPlan> plans;
     std::list<nb::CachedSchedule> schedules;
+    std::list<nb::CachedSchedule> retired;  // evicted while pinned by a CUDA graph
     // Repeat fast path: the previous stand-alone all-to-allv (buffers, counts;
     // nvswitch model) and the cached schedule it launched.  Cleared whenever
     // schedules, windows or the config change.
@@ -249,6 +286,7 @@ struct nimbleComm {
     nb::RankBuffers last_rb;
     cudaStream_t bench_stream = nullptr;
     uint64_t* d_trace = nullptr;  // NIMBLE_TRACE=1: device timeline of the last launch
+    nb::DeviceStats* d_stats = nullptr;  // NIMBLE_STATS=1: per-kind byte counters, slot occupancy
     cudaEvent_t last_launch = nullptr;  // launches on one comm are serialized across streams
     cudaStream_t last_stream = nullptr;
     bool launched = false;
@@ -263,6 +301,24 @@ namespace {
 
 struct Clique {
     std::vector<nimbleComm*> comms;
+    struct Region {
+        int device;
+        uint8_t* ctrl;
+        uint8_t* staging;
+    };
+    std::vector<Region> deferred;  // ctrl / staging of destroyed members
+    ~Clique() {
+        int prev = -1;
+        cudaGetDevice(&prev);
+        for (const Region& r : deferred) {
+            if (cudaSetDevice(r.device) != cudaSuccess) continue;
+            cudaDeviceSynchronize();
+            cudaFree(r.ctrl);
+            cudaFree(r.staging);
+        }
+        cudaGetLastError();
+        if (prev >= 0) cudaSetDevice(prev);
+    }
 };
 
 void upload_view(nimbleComm* c) {
@@ -276,6 +332,7 @@ void upload_view(nimbleComm* c) {
     c->view.nwin = static_cast<uint32_t>(c->windows.size());
     c->view.status = c->d_status;
     c->view.scratch = c->d_scratch;
+    c->view.stats = c->d_stats;
     c->view.epoch = c->d_epoch;
     const char* t = std::getenv("NIMBLE_TIMEOUT_MS");
     c->view.timeout_ms = t && *t ? static_cast<uint32_t>(std::atoi(t)) : 60000u;
@@ -321,6 +378,22 @@ void default_config(nimbleCommConfig* cfg, int nranks) {
     cfg->ll_max = kLLMaxData;
 }
 
+// Peer access from the current device to `dev` (idempotent).
+void enable_peer(int dev) {
+    cudaError_t e = cudaDeviceEnablePeerAccess(dev, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    else CUDA_TRY(e);
+}
+
+// Default CTAs per launch.  A device hosting k ranks of this comm (one
+// process, k streams) runs k engine grids at once, and each grid's producers
+// spin on flags raised by the others: all of them must be resident together,
+// so each takes (SMs - k) / k CTAs -- one SM per rank to spare for the next
+// stream-ordered grid's early CTAs and any other kernel on the device.
+void set_share(nimbleComm* c) {
+    c->sms_share = c->colocated <= 1 ? c->sms : std::max(1, (c->sms - c->colocated) / c->colocated);
+}
+
 // Allocate ctrl + staging, exchange handles / pointers, map peers.
 void setup_regions(nimbleComm* c, bool single_process) {
     DeviceGuard g(c->device);
@@ -338,14 +411,36 @@ void setup_regions(nimbleComm* c, bool single_process) {
     mine.pid = ::getpid();
     mine.dev = c->device;
     mine.host = ::gethostid();
+    mine.ctrl_ptr = reinterpret_cast<uint64_t>(c->ctrl);
+    mine.staging_ptr = reinterpret_cast<uint64_t>(c->staging);
     CUDA_TRY(cudaIpcGetMemHandle(&mine.ctrl, c->ctrl));
     CUDA_TRY(cudaIpcGetMemHandle(&mine.staging, c->staging));
     std::vector<PeerInfo> all(static_cast<size_t>(c->nranks));
     c->boot->allgather(&mine, sizeof mine, all.data());
+    c->colocated = 0;
+    for (int r = 0; r < c->nranks; ++r) {
+        const PeerInfo& p = all[static_cast<size_t>(r)];
+        if (p.host != mine.host) throw Error(nimbleInvalidUsage, "comm: ranks must share one NVLink box");
+        if (p.dev == mine.dev) {
+            // ranks sharing a device must share a process (streams of one
+            // context run concurrently; separate processes time-slice, and
+            // the engines' flag waits would stall)
+            if (p.pid != mine.pid)
+                throw Error(nimbleInvalidUsage, "comm: ranks on one GPU must live in one process (one thread each)");
+            ++c->colocated;
+        }
+    }
     for (int r = 0; r < c->nranks; ++r) {
         if (r == c->rank) continue;
         const PeerInfo& p = all[static_cast<size_t>(r)];
-        if (p.host != mine.host) throw Error(nimbleInvalidUsage, "comm: ranks must share one NVLink box");
+        if (p.pid == mine.pid) {
+            // a rank of this process (one thread per rank): its pointers are
+            // valid here as they are, given peer access to its device
+            if (p.dev != mine.dev) enable_peer(p.dev);
+            c->peer_ctrl[static_cast<size_t>(r)] = reinterpret_cast<uint8_t*>(p.ctrl_ptr);
+            c->peer_staging[static_cast<size_t>(r)] = reinterpret_cast<uint8_t*>(p.staging_ptr);
+            continue;
+        }
         void* a = nullptr;
         void* b = nullptr;
         CUDA_TRY(cudaIpcOpenMemHandle(&a, p.ctrl, cudaIpcMemLazyEnablePeerAccess));
@@ -355,6 +450,7 @@ void setup_regions(nimbleComm* c, bool single_process) {
         c->peer_ctrl[static_cast<size_t>(r)] = static_cast<uint8_t*>(a);
         c->peer_staging[static_cast<size_t>(r)] = static_cast<uint8_t*>(b);
     }
+    set_share(c);
 }
 
 void setup_common(nimbleComm* c) {
@@ -374,6 +470,10 @@ void setup_common(nimbleComm* c) {
     CUDA_TRY(cudaEventCreateWithFlags(&c->last_launch, cudaEventDisableTiming));
     if (const char* t = std::getenv("NIMBLE_TRACE"); t && *t == '1')
         CUDA_TRY(cudaMalloc(&c->d_trace, sizeof(uint64_t) * kTraceSlots));
+    if (const char* t = std::getenv("NIMBLE_STATS"); t && *t == '1') {
+        CUDA_TRY(cudaMalloc(&c->d_stats, sizeof(DeviceStats)));
+        CUDA_TRY(cudaMemset(c->d_stats, 0, sizeof(DeviceStats)));
+    }
     c->win_table.assign(static_cast<size_t>(kMaxWindows) * kMaxRanks, 0);
 }
 
@@ -384,6 +484,19 @@ void free_regions(nimbleComm* c) {
     if (c->ctrl) cudaFree(c->ctrl);
     if (c->staging) cudaFree(c->staging);
     c->ctrl = c->staging = nullptr;
+}
+
+// Wait until no launch of this comm is in flight.  A device hosting one rank
+// syncs the device (graph replays included).  A device hosting several ranks
+// of the comm waits for this comm's last eager launch only: a device-wide
+// sync there would also wait for peer grids that may be waiting for this
+// rank's next launch (graph replays must be synchronized by the caller).
+void quiesce(nimbleComm* c) {
+    if (c->colocated > 1) {
+        if (c->launched) CUDA_TRY(cudaEventSynchronize(c->last_launch));
+    } else {
+        CUDA_TRY(cudaDeviceSynchronize());
+    }
 }
 
 // ---------------------------------------------------------------- planning
@@ -567,6 +680,9 @@ void fill_posts(nimbleComm* c, RankBuffers& rb, const PlanResult& plan) {
     }
 }
 
+constexpr size_t kCachedSchedules = 4;
+void reap_retired(nimbleComm* c);
+
 CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& plan, const RankBuffers& rb,
                              cudaStream_t st) {
     std::vector<uint64_t> key = {plan_id, c->cfg.pipe_chunk, c->cfg.p2p_buffer,
@@ -593,21 +709,35 @@ CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& 
         throw Error(nimbleInvalidUsage, "graph capture: run the same exchange once before capturing it "
                                         "(its schedule must be cached; capture does not allow uploads)");
     c->fast.cs = nullptr;  // entries may be recycled below
+    reap_retired(c);
     CachedSchedule cs;
     cs.key = key;
     const uint64_t dchunk = c->cfg.direct_chunk ? c->cfg.direct_chunk : kDefaultDirectChunk;
     cs.sc = build_schedule(plan, rb, c->cfg.pipe_chunk, slot_count(c->cfg), dchunk,
                            c->cfg.push_chunk ? c->cfg.push_chunk : kDefaultPushChunk, c->cfg.ll_max);
-    if (c->schedules.size() >= 4) {  // recycle the oldest entry's device buffers
-        CUDA_TRY(cudaDeviceSynchronize());  // no launch may still read them
-        CachedSchedule& old = c->schedules.back();
-        cs.items = std::move(old.items);
-        cs.posts = std::move(old.posts);
-        cs.send_posts = std::move(old.send_posts);
-        cs.finals = std::move(old.finals);
-        cs.ll_items = std::move(old.ll_items);
-        c->schedules.pop_back();
+    // Recycle the least recently used entry that no CUDA graph holds, once
+    // kCachedSchedules of them exist: wait for its own last launch (its event,
+    // not a device-wide sync) and reuse its device buffers.
+    size_t unpinned = 0;
+    for (const CachedSchedule& e : c->schedules) unpinned += !e.pinned();
+    if (unpinned >= kCachedSchedules) {
+        for (auto it = std::prev(c->schedules.end());; --it) {
+            if (!it->pinned()) {
+                it->wait_idle();
+                cs.items = std::move(it->items);
+                cs.posts = std::move(it->posts);
+                cs.send_posts = std::move(it->send_posts);
+                cs.finals = std::move(it->finals);
+                cs.ll_items = std::move(it->ll_items);
+                std::swap(cs.used, it->used);
+                if (c->last_cs == &*it) c->last_cs = nullptr;
+                c->schedules.erase(it);
+                break;
+            }
+            if (it == c->schedules.begin()) break;
+        }
     }
+    if (!cs.used) CUDA_TRY(cudaEventCreateWithFlags(&cs.used, cudaEventDisableTiming));
     cs.items.assign(cs.sc.items, st);
     cs.posts.assign(cs.sc.posts, st);
     cs.send_posts.assign(cs.sc.send_posts, st);
@@ -615,6 +745,60 @@ CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& 
     cs.ll_items.assign(cs.sc.ll_items, st);
     c->schedules.push_front(std::move(cs));
     return c->schedules.front();
+}
+
+// Drop every cached schedule (config change, deregistration, bench scope).
+// Entries a CUDA graph still holds move to `retired` and stay allocated until
+// the last such graph is destroyed; the rest are released once idle.
+void drop_schedules(nimbleComm* c) {
+    for (auto it = c->schedules.begin(); it != c->schedules.end();) {
+        auto next = std::next(it);
+        if (it->pinned()) c->retired.splice(c->retired.end(), c->schedules, it);
+        else it->wait_idle();
+        it = next;
+    }
+    c->schedules.clear();
+    c->fast.cs = c->last_cs = nullptr;
+}
+
+// Free retired entries whose graphs are all gone.
+void reap_retired(nimbleComm* c) {
+    for (auto it = c->retired.begin(); it != c->retired.end();) {
+        if (it->pinned()) {
+            ++it;
+        } else {
+            it->wait_idle();
+            it = c->retired.erase(it);
+        }
+    }
+}
+
+// A launch being captured into a CUDA graph keeps raw pointers to the
+// entry's device buffers: pin the entry for the graph's lifetime (a user
+// object retained by the graph decrements the pin count when the graph and
+// all its executable instances are destroyed).
+void pin_for_capture(CachedSchedule& cs, cudaStream_t st) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaGraph_t graph = nullptr;
+    CUDA_TRY(cudaStreamGetCaptureInfo(st, &cap, nullptr, &graph, nullptr, nullptr));
+    if (cap != cudaStreamCaptureStatusActive || !graph) return;
+    auto* hold = new std::shared_ptr<GraphPins>(cs.pins);
+    (*hold)->n.fetch_add(1);
+    cudaUserObject_t obj = nullptr;
+    cudaError_t e = cudaUserObjectCreate(
+        &obj, hold,
+        [](void* p) {
+            auto* h = static_cast<std::shared_ptr<GraphPins>*>(p);
+            (*h)->n.fetch_sub(1);
+            delete h;
+        },
+        1, cudaUserObjectNoDestructorSync);
+    if (e != cudaSuccess) {
+        (*hold)->n.fetch_sub(1);
+        delete hold;
+        CUDA_TRY(e);
+    }
+    CUDA_TRY(cudaGraphRetainUserObject(graph, obj, 1, cudaGraphUserObjectMove));
 }
 
 void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream_t st) {
@@ -652,7 +836,7 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
         CUDA_TRY(cudaMemcpyAsync(c->d_trace, init, sizeof init, cudaMemcpyHostToDevice, st));
         a.trace = c->d_trace;
     }
-    int ctas = c->cfg.ctas > 0 ? c->cfg.ctas : c->sms;
+    int ctas = c->cfg.ctas > 0 ? c->cfg.ctas : c->sms_share;
     // small exchanges: no more CTAs than items (each CTA costs a fence at exit)
     const size_t work = cs.sc.items.size() + cs.sc.ll_items.size();
     ctas = std::max(1, std::min({ctas, c->sms, static_cast<int>(std::max<size_t>(work, 1))}));
@@ -669,8 +853,11 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     CUDA_TRY(launch_exchange(a, ctas, st));
     if (eager) {
         CUDA_TRY(cudaEventRecord(c->last_launch, st));
+        CUDA_TRY(cudaEventRecord(cs.used, st));
         c->last_stream = st;
         c->launched = true;
+    } else {
+        pin_for_capture(cs, st);
     }
 }
 
@@ -771,8 +958,8 @@ void* register_window(nimbleComm* c, void* buff, size_t size) {
     if (c->boot) {
         struct Blob {
             cudaIpcMemHandle_t h;
-            uint64_t offset, size;
-            int32_t live, pad;
+            uint64_t offset, size, addr;
+            int32_t live, pid;
         } mine{};
         if (w.live) {
             auto [base, asz] = allocation_of(buff);
@@ -782,6 +969,8 @@ void* register_window(nimbleComm* c, void* buff, size_t size) {
         }
         mine.size = size;
         mine.live = w.live;
+        mine.addr = w.base;
+        mine.pid = ::getpid();
         std::vector<Blob> all(static_cast<size_t>(c->nranks));
         c->boot->allgather(&mine, sizeof mine, all.data());
         for (int r = 0; r < c->nranks; ++r) {
@@ -789,6 +978,8 @@ void* register_window(nimbleComm* c, void* buff, size_t size) {
             uint64_t addr = 0;
             if (r == c->rank) {
                 addr = w.base;
+            } else if (b.live && b.pid == mine.pid) {
+                addr = b.addr;  // a rank of this process: its pointer as it is
             } else if (b.live) {
                 void* p = ipc_cache().acquire(b.h);
                 w.opened.push_back(p);
@@ -850,8 +1041,7 @@ void bench_matrix(nimbleComm* c, const std::vector<uint64_t>& m, int warmup, int
                 for (void* p : c->windows[k].opened) ipc_cache().release(p);
                 c->windows[k].opened.clear();
             }
-            c->schedules.clear();
-            c->fast.cs = c->last_cs = nullptr;
+            drop_schedules(c);
             for (void* b : bufs) cudaFree(b);
         }
     } scope{c, {}, c->windows.size()};
@@ -998,15 +1188,14 @@ nimbleResult_t nimbleCommInitAll(nimbleComm_t* comms, int ndev, const int* devli
         }
         for (auto& c : made) {
             nb::DeviceGuard g(c->device);
+            c->colocated = 0;
             for (auto& p : made) {
                 c->peer_ctrl[static_cast<size_t>(p->rank)] = p->ctrl;
                 c->peer_staging[static_cast<size_t>(p->rank)] = p->staging;
-                if (p->device != c->device) {
-                    cudaError_t e = cudaDeviceEnablePeerAccess(p->device, 0);
-                    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
-                    else CUDA_TRY(e);
-                }
+                if (p->device != c->device) nb::enable_peer(p->device);
+                else ++c->colocated;  // a repeated device: co-resident ranks
             }
+            nb::set_share(c.get());
             nb::upload_view(c.get());
         }
         for (int r = 0; r < ndev; ++r) comms[r] = made[static_cast<size_t>(r)].release();
@@ -1023,14 +1212,26 @@ nimbleComm::~nimbleComm() {
     for (nb::Window& w : windows)
         for (void* p : w.opened) nb::ipc_cache().release(p);
     windows.clear();
+    for (auto& e : schedules) e.wait_idle();
+    for (auto& e : retired) e.wait_idle();
     schedules.clear();
+    retired.clear();
     fast.cs = last_cs = nullptr;
+    if (clique) {
+        // Peers' engine grids of this clique write into my ctrl region at
+        // their epilogue (done / pulled / LL acks) whether or not they
+        // exchanged data with me: the regions outlive me until the last
+        // member of the clique is gone (~Clique syncs every device first).
+        clique->deferred.push_back({device, ctrl, staging});
+        ctrl = staging = nullptr;
+    }
     nb::free_regions(this);
     cudaFree(d_view);
     cudaFree(d_win_table);
     cudaFree(d_scratch);
     cudaFree(d_epoch);
     if (d_trace) cudaFree(d_trace);
+    if (d_stats) cudaFree(d_stats);
     if (h_status) cudaFreeHost(h_status);
     if (bench_stream) cudaStreamDestroy(bench_stream);
     if (last_launch) cudaEventDestroy(last_launch);
@@ -1043,7 +1244,7 @@ nimbleResult_t nimbleCommDestroy(nimbleComm_t c) {
     return guarded([&] {
         {
             nb::DeviceGuard g(c->device);
-            cudaDeviceSynchronize();
+            nb::quiesce(c);
             if (c->boot) c->boot->barrier();  // nobody touches my regions any more
         }
         if (c->clique) {
@@ -1107,7 +1308,7 @@ nimbleResult_t nimbleCommSetConfig(nimbleComm_t c, const nimbleCommConfig* cfg) 
         if (regrow && c->clique)
             throw nb::Error(nimbleInvalidUsage, "config: staging geometry is fixed for single-process comms");
         if (regrow) {
-            CUDA_TRY(cudaDeviceSynchronize());
+            nb::quiesce(c);
             if (c->boot) c->boot->barrier();
             nb::free_regions(c);  // nulls the pointers: a failing setup below leaves nothing to double-free
             c->cfg = next;
@@ -1117,8 +1318,7 @@ nimbleResult_t nimbleCommSetConfig(nimbleComm_t c, const nimbleCommConfig* cfg) 
         }
         c->cfg = next;
         c->plans.clear();
-        c->schedules.clear();
-        c->fast.cs = c->last_cs = nullptr;
+        nb::drop_schedules(c);
         if (c->boot) c->boot->barrier();
     });
 }
@@ -1143,13 +1343,12 @@ nimbleResult_t nimbleCommDeregister(const nimbleComm_t c, void* handle) {
         const size_t id = reinterpret_cast<uintptr_t>(handle) - 1;
         if (id >= c->windows.size() || !c->windows[id].live) throw nb::Error(nimbleInvalidArgument, "bad handle");
         nb::DeviceGuard g(c->device);
-        CUDA_TRY(cudaDeviceSynchronize());
+        nb::quiesce(c);
         if (c->boot) c->boot->barrier();
         for (void* p : c->windows[id].opened) nb::ipc_cache().release(p);
         c->windows[id].opened.clear();
         c->windows[id].live = false;
-        c->schedules.clear();
-        c->fast.cs = c->last_cs = nullptr;
+        nb::drop_schedules(c);
     });
 }
 
@@ -1293,8 +1492,20 @@ nimbleResult_t nimbleCommDebugTrace(nimbleComm_t c, uint64_t* out, int n) {
         if (!c || !out || n < nb::kTraceSlots) throw nb::Error(nimbleInvalidArgument, "trace: bad argument");
         if (!c->d_trace) throw nb::Error(nimbleInvalidUsage, "trace: set NIMBLE_TRACE=1 before creating the comm");
         nb::DeviceGuard g(c->device);
-        CUDA_TRY(cudaDeviceSynchronize());
+        nb::quiesce(c);
         CUDA_TRY(cudaMemcpy(out, c->d_trace, sizeof(uint64_t) * nb::kTraceSlots, cudaMemcpyDeviceToHost));
+    });
+}
+
+nimbleResult_t nimbleCommGetStats(nimbleComm_t c, nimbleCommStats* out, int reset) {
+    return guarded([&] {
+        if (!c || !out) throw nb::Error(nimbleInvalidArgument, "stats: null argument");
+        if (!c->d_stats) throw nb::Error(nimbleInvalidUsage, "stats: set NIMBLE_STATS=1 before creating the comm");
+        static_assert(sizeof(nimbleCommStats) == sizeof(nb::DeviceStats), "stats layout");
+        nb::DeviceGuard g(c->device);
+        nb::quiesce(c);
+        CUDA_TRY(cudaMemcpy(out, c->d_stats, sizeof *out, cudaMemcpyDeviceToHost));
+        if (reset) CUDA_TRY(cudaMemset(c->d_stats, 0, sizeof(nb::DeviceStats)));
     });
 }
 

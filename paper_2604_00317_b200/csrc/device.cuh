@@ -126,7 +126,39 @@ struct FlagLayout {
     __host__ __device__ static constexpr uint64_t ll_off(int R, int e, int s) {
         return flags_end(R) + (static_cast<uint64_t>(e) * R + s) * kLLSlotBytes;
     }
-    __host__ __device__ static constexpr uint64_t bytes(int R) { return ll_off(R, 2, 0); }
+    // Slot-occupancy counters of ring (s, d) hosted here (NIMBLE_STATS=1): a
+    // count of claimed-not-released slots and one word per slot, claimed by
+    // the stager after its consumed-flag wait and released by the forwarder
+    // before it raises the consumed flag.  The bounded-buffer invariant of
+    // the reference (tests/acceptance.cpp:270-288: occupancy <= S) is checked
+    // on the device from these.
+    __host__ __device__ static constexpr uint64_t occ_count_off(int R, int s, int d) {
+        return ll_off(R, 2, 0) + 4ull * ((static_cast<uint64_t>(s) * R + d) * (kMaxSlots + 1));
+    }
+    __host__ __device__ static constexpr uint64_t bytes(int R) {
+        return (occ_count_off(R, R - 1, R) + 255) / 256 * 256;  // one past the last ring
+    }
+};
+
+// Per-rank device counters (NIMBLE_STATS=1 at comm creation; nimbleCommGetStats).
+enum StatKind : int {
+    kStatLocal = 0,
+    kStatPush = 1,     // by receiver: bytes pushed (zero copy or into its self ring)
+    kStatStage = 2,    // by relay: bytes staged into a relay's ring (hop 1)
+    kStatForward = 3,  // by final receiver: bytes forwarded out of a ring hosted here (hop 2)
+    kStatPull = 4,     // by sender: bytes pulled out of its registered segment
+    kStatLLSend = 5,   // by receiver
+    kStatLLRecv = 6,   // by sender
+    kStatDrain = 7,    // by sender: bytes drained from my self ring (staged receive)
+    kStatKinds = 8,
+};
+struct DeviceStats {
+    unsigned long long bytes[kStatKinds][kMaxRanks];
+    unsigned long long items[kStatKinds][kMaxRanks];
+    unsigned long long occ_max;      // max over my stager claims of the ring's claimed-slot count
+    unsigned long long occ_double;   // claims of a slot still held by an undrained chunk (must stay 0)
+    unsigned long long occ_claims;   // ring-slot claims made
+    unsigned long long pad;
 };
 
 // Comm-lifetime device view (set up once at init / registration).
@@ -139,6 +171,7 @@ struct CommDevice {
     uint32_t timeout_ms;
     uint32_t* status;             // host-mapped: [0] error code, [1] detail
     uint64_t* epoch;              // launches completed on this comm (advanced by each launch's last CTA)
+    DeviceStats* stats;           // null unless NIMBLE_STATS=1
     uint32_t* scratch;            // [0] queue head, [1] CTAs done, [2, 2+kMaxRanks) grant decisions
                                   // as sender, [2+kMaxRanks, 2+2*kMaxRanks) as receiver (kDecide*)
 };

@@ -190,6 +190,8 @@ struct StageDesc {
     uint64_t tag1;
     uint64_t* flag2;
     uint64_t tag2;
+    uint32_t* occ;  // NIMBLE_STATS: the drained ring's claimed-slot count (slot word at occ + 1 + occ_slot)
+    uint32_t occ_slot;
 };
 
 // Item-end actions handed from the consumers to the signal warp, which does
@@ -200,6 +202,8 @@ struct SigDesc {
     uint64_t tag1;
     uint64_t* flag2;
     uint64_t tag2;
+    uint32_t* occ;
+    uint32_t occ_slot;
 };
 
 struct SharedState {
@@ -357,6 +361,23 @@ __device__ __forceinline__ uint64_t* ctrl_flag(const LaunchArgs& a, int rank, ui
     return reinterpret_cast<uint64_t*>(a.comm->ctrl[rank] + off);
 }
 
+// NIMBLE_STATS: stager side of the slot-occupancy check (FlagLayout).  Runs
+// after the consumed-flag acquire, so the forwarder's release of chunk
+// seq - S (done before it raised that flag) is visible here.
+__device__ void claim_slot(const CommDevice* c, int host, int s, int d, uint32_t slot, uint32_t seq) {
+    auto* cnt = reinterpret_cast<unsigned int*>(c->ctrl[host] + FlagLayout::occ_count_off(c->nranks, s, d));
+    const unsigned int prev = atomicExch_system(cnt + 1 + slot, seq + 1);
+    const unsigned int occ = atomicAdd_system(cnt, 1u) + 1;
+    if (prev) atomicAdd(&c->stats->occ_double, 1ull);
+    atomicAdd(&c->stats->occ_claims, 1ull);
+    atomicMax(&c->stats->occ_max, static_cast<unsigned long long>(occ));
+}
+
+__device__ __forceinline__ void count_item(const CommDevice* c, int kind, int peer, uint64_t bytes) {
+    atomicAdd(&c->stats->bytes[kind][peer], static_cast<unsigned long long>(bytes));
+    atomicAdd(&c->stats->items[kind][peer], 1ull);
+}
+
 enum Prep { kGo, kSkip };
 
 // Producer: the item's source, destination and end-of-item actions.  kSkip
@@ -394,6 +415,7 @@ __device__ Prep prepare(SharedState& sh, const LaunchArgs& a, const Item& it, ui
             !wait_ge(ctrl_flag(a, me, FlagLayout::consumed_off(R, d, host, slot)), tag_of(a.epoch, it.seq - a.slots), c,
                      kErrSlotTimeout))
             return kSkip;
+        if (c->stats) claim_slot(c, host, me, d, slot, it.seq);
         dst = reinterpret_cast<uint64_t>(ring_slot(a, host, me, d, it.seq));
         end.action = kActRelease1;  // chunk landed in the slot: raise its ready flag
         end.flag1 = ctrl_flag(a, host, FlagLayout::ready_off(R, me, d, slot));
@@ -415,6 +437,8 @@ __device__ Prep prepare(SharedState& sh, const LaunchArgs& a, const Item& it, ui
     end.action = kActRelease2;  // the slot is drained: hand it back to the stager
     end.flag2 = ctrl_flag(a, s, FlagLayout::consumed_off(R, d, me, slot));
     end.tag2 = tag_of(a.epoch, it.seq);
+    end.occ = c->stats ? reinterpret_cast<uint32_t*>(c->ctrl[me] + FlagLayout::occ_count_off(R, s, d)) : nullptr;
+    end.occ_slot = slot;
     if (d == me) {
         dst = a.posts[s].off + it.dst;  // staged self receive: absolute local address
         return kGo;
@@ -492,6 +516,7 @@ __device__ void ll_send_all(const LaunchArgs& a) {
             const uint8_t* src = reinterpret_cast<const uint8_t*>(it.src);
             const uint32_t n = it.bytes, lines = (n + 7) / 8;
             if (it.seq == 0 && threadIdx.x == 0) st_ll(slot, it.pad, ~it.pad, flag);
+            if (threadIdx.x == 0 && c->stats) count_item(c, kStatLLSend, d, it.bytes);
             for (uint32_t k = threadIdx.x; k < lines; k += blockDim.x) {
                 const uint32_t off = 8 * k, m = n - off < 8 ? n - off : 8;
                 const uint64_t v = load_upto8(src + off, m);
@@ -519,6 +544,7 @@ __device__ void ll_recv_all(const LaunchArgs& a) {
         const uint4* lines0 = slot + 1 + it.seq * (kLLPiece / 8);
         uint8_t* dst = reinterpret_cast<uint8_t*>(it.dst);
         const uint32_t n = it.bytes, lines = (n + 7) / 8;
+        if (threadIdx.x == 0 && c->stats) count_item(c, kStatLLRecv, s, n);
         // thread slot k = lines is piece 0's header check (line 0)
         const uint32_t last = it.seq == 0 ? lines : lines - 1;
         for (uint32_t k = threadIdx.x; k <= last; k += blockDim.x) {
@@ -588,6 +614,13 @@ __device__ void produce(SharedState& sh, uint8_t* stages, const LaunchArgs& a) {
             sd.tag1 = end.tag1;
             sd.flag2 = end.flag2;
             sd.tag2 = end.tag2;
+            sd.occ = end.occ;
+            sd.occ_slot = end.occ_slot;
+        }
+        if (a.comm->stats) {
+            const int me = a.comm->rank;
+            const int kind = it.kind == kForward ? (it.peer == me ? kStatDrain : kStatForward) : it.kind;
+            count_item(a.comm, kind, kind == kStatDrain ? it.aux : it.peer, it.bytes);
         }
         // head: bytes until the destination is 16-byte aligned
         uint64_t n = it.bytes;
@@ -666,6 +699,10 @@ __device__ void signal_loop(SharedState& sh) {
         mbar_wait(&sh.sig_full[j], (n / kSig) & 1);
         const SigDesc sd = sh.sig[j];
         if (sd.terminate) break;
+        if (sd.occ) {  // NIMBLE_STATS: release the drained slot before handing it back
+            atomicExch_system(sd.occ + 1 + sd.occ_slot, 0u);
+            atomicSub_system(sd.occ, 1u);
+        }
         asm volatile("fence.acq_rel.sys;" ::: "memory");  // the item's bytes before its flag
         if (sd.action & kActRelease1) st_relaxed(sd.flag1, sd.tag1);
         if (sd.action & kActRelease2) st_relaxed(sd.flag2, sd.tag2);

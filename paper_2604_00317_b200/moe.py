@@ -75,8 +75,23 @@ class MoEDispatcher:
             acc += c
         return out
 
+    @staticmethod
+    def _enter(stream):
+        """Exchanges on `stream` see the current stream's work (buffers filled)."""
+        if stream is not None:
+            stream.wait_stream(torch.cuda.current_stream())
+
+    @staticmethod
+    def _leave(stream):
+        """The current stream sees the exchanges' results."""
+        if stream is not None:
+            torch.cuda.current_stream().wait_stream(stream)
+
     def dispatch(self, x: torch.Tensor, topk_ids: torch.Tensor, stream=None):
-        """x [T, H], topk_ids [T, k] (int) -> (recv_x [N, H], recv_expert [N] local ids, handle)."""
+        """x [T, H], topk_ids [T, k] (int) -> (recv_x [N, H], recv_expert [N] local ids, handle).
+        `stream` (optional, a torch.cuda.Stream): run the exchanges there; it is
+        ordered after the current stream's work and before the current stream's
+        later work."""
         T, k = topk_ids.shape
         if T * k > self.cap_send:
             raise ValueError("more assignments than the dispatcher's capacity")
@@ -88,7 +103,10 @@ class MoEDispatcher:
         self.send_ids[:n] = (flat[order] % self.experts_per_rank).to(torch.int32)
         self.count_out.copy_(torch.bincount(dest, minlength=self.R))
         # counts first (one int64 per peer), then the rows
+        self._enter(stream)
         self.comm.alltoall(self.count_out, self.count_in, 8, stream)
+        if stream is not None:
+            stream.synchronize()  # the counts are read on the host next
         send_counts = self.count_out.tolist()
         recv_counts = self.count_in.tolist()
         if sum(recv_counts) > self.cap_recv:
@@ -99,6 +117,7 @@ class MoEDispatcher:
         si = [c * 4 for c in send_counts]
         ri = [c * 4 for c in recv_counts]
         self.comm.alltoallv(self.send_ids, si, self._displs(si), self.recv_ids, ri, self._displs(ri), stream)
+        self._leave(stream)
         m = sum(recv_counts)
         return self.recv_buf[:m], self.recv_ids[:m], DispatchHandle(order, send_counts, recv_counts, T, k)
 
@@ -109,7 +128,9 @@ class MoEDispatcher:
             self.recv_buf[:m].copy_(y)
         sb = [c * self.row for c in handle.recv_counts]
         rb = [c * self.row for c in handle.send_counts]
+        self._enter(stream)
         self.comm.alltoallv(self.recv_buf, sb, self._displs(sb), self.back_buf, rb, self._displs(rb), stream)
+        self._leave(stream)
         n = handle.num_tokens * handle.topk
         back = self.back_buf[:n]
         if weights is not None:

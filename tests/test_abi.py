@@ -78,7 +78,8 @@ def test_ctypes_structs_match_the_header_layout(tmp_path):
     program compiled against include/nimble.h prints them)."""
     pairs = [(_lib.PlannerConfig, "nimblePlannerConfig"), (_lib.PlanStats, "nimblePlanStats"),
              (_lib.CommConfig, "nimbleCommConfig"), (_lib.UniqueId, "nimbleUniqueId"),
-             (_lib.Item, "nimbleItem"), (_lib.BenchResult, "nimbleBenchResult")]
+             (_lib.Item, "nimbleItem"), (_lib.BenchResult, "nimbleBenchResult"),
+             (_lib.CommStats, "nimbleCommStats")]
     lines = ['#include <stddef.h>', '#include <stdio.h>', '#include "nimble.h"', "int main(void) {"]
     for cls, cname in pairs:
         lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')

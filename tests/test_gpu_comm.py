@@ -1,23 +1,76 @@
-"""Multi-GPU parity of the NVLink data path (one process per GPU, spawned).
+"""Parity of the NVLink data path, bit-exact against the payload function
+and the host oracle (oracle/cpu_exchange.c orc_alltoallv).
 
-Runs only on a box with >= 2 GPUs (gpurun --gpus 2|4); every check is
-bit-exact against the payload function / the host oracle.
+Two ways to run R ranks:
+  - "proc": one process per GPU (gpurun --gpus 2|4), the production layout;
+  - "thread": R ranks co-resident on ONE GPU -- one process, one thread and
+    one stream per rank, nimbleCommInitRank over the same bootstrap.  The comm
+    sizes every rank's engine grid to (SMs - R) / R CTAs so all R grids are
+    resident at once; peers' ctrl / staging / registered windows are plain
+    pointers into the same HBM.  Every part of the cross-rank protocol runs
+    (posts, ready / consumed ring flags, pushes, TMA pulls, LL slots, relay
+    rings, completion counters) -- only the wire is HBM instead of NVLink.
+    This is how a 1-GPU box runs the 2/4/8-rank protocol tests.
 """
 import os
 import socket
+import threading
+import traceback
 
 import pytest
 
 torch = pytest.importorskip("torch")
 
-pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+pytestmark = [pytest.mark.gpu]
 
 MiB = 1 << 20
+_CALL_TIMEOUT_S = 600
 
 
 def _ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
+
+# ---------------------------------------------------------------- rank context
+
+_CTX = threading.local()  # .mode ("proc" | "thread"), .barrier (thread mode)
+
+
+def _sync():
+    """Wait for this rank's work.  In thread mode only the rank's own stream:
+    a device-wide sync would also wait for peer grids that may be waiting for
+    this rank's next launch."""
+    if getattr(_CTX, "mode", "proc") == "thread":
+        torch.cuda.current_stream().synchronize()
+    else:
+        torch.cuda.synchronize()
+
+
+def _barrier():
+    if getattr(_CTX, "mode", "proc") == "thread":
+        _CTX.barrier.wait(timeout=_CALL_TIMEOUT_S)
+    else:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def _capture(fn):
+    """CUDA-graph capture of fn() on a private stream, thread-local capture mode
+    (other ranks' threads keep running), no device-wide sync."""
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        g.capture_begin(capture_error_mode="thread_local")
+        try:
+            fn()
+        finally:
+            g.capture_end()
+    torch.cuda.current_stream().wait_stream(s)
+    return g
+
+
+# ---------------------------------------------------------------- process mode
 
 def _free_port():
     s = socket.socket()
@@ -37,7 +90,7 @@ def _spawn(fn, world, *args):
         p.start()
     out = {}
     for _ in procs:
-        rank, res = q.get(timeout=600)
+        rank, res = q.get(timeout=_CALL_TIMEOUT_S)
         out[rank] = res
     for p in procs:
         p.join(timeout=120)
@@ -48,12 +101,13 @@ def _spawn(fn, world, *args):
 
 
 def _entry(fn, rank, world, port, q, args):
-    import traceback
     try:
-        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), NIMBLE_TIMEOUT_MS="15000")
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), NIMBLE_TIMEOUT_MS="15000",
+                          NIMBLE_STATS="1")
         import torch.distributed as dist
         torch.cuda.set_device(rank)
         dist.init_process_group("gloo", rank=rank, world_size=world)
+        _CTX.mode = "proc"
         from paper_2604_00317_b200 import comm as C
         uid = [C.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, 0)
@@ -67,7 +121,161 @@ def _entry(fn, rank, world, port, q, args):
         q.put((rank, "ERROR " + traceback.format_exc()))
 
 
-def _exchange_and_check(comm, rank, R, m, register, seed, register_send=False):
+# ---------------------------------------------------------------- thread mode (co-resident on GPU 0)
+
+def _thread_server(R, conn):
+    """Long-lived child process: runs worker calls as R threads on GPU 0."""
+    os.environ.update(NIMBLE_TIMEOUT_MS="15000", NIMBLE_STATS="1")
+    torch.cuda.set_device(0)
+    from paper_2604_00317_b200 import comm as C
+    while True:
+        msg = conn.recv()
+        if msg is None:
+            break
+        fn, args = msg
+        uid = C.unique_id()
+        barrier = threading.Barrier(R)
+        out = [None] * R
+
+        def run(rank):
+            try:
+                torch.cuda.set_device(0)
+                _CTX.mode, _CTX.barrier = "thread", barrier
+                s = torch.cuda.Stream()
+                with torch.cuda.stream(s):
+                    comm = C.Comm.init_rank(R, uid, rank)
+                    out[rank] = globals()[fn](comm, rank, R, *args)
+                    s.synchronize()
+                    barrier.wait(timeout=_CALL_TIMEOUT_S)
+                    comm.destroy()
+            except Exception:
+                out[rank] = "ERROR " + traceback.format_exc()
+                barrier.abort()
+
+        threads = [threading.Thread(target=run, args=(r,), daemon=True) for r in range(R)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        conn.send(out)
+
+
+_SERVERS = {}
+
+
+def _server(R):
+    import multiprocessing as mp
+    srv = _SERVERS.get(R)
+    if srv is None or not srv[0].is_alive():
+        ctx = mp.get_context("spawn")
+        parent, child = ctx.Pipe()
+        p = ctx.Process(target=_thread_server, args=(R, child), daemon=True)
+        p.start()
+        srv = _SERVERS[R] = (p, parent)
+    return srv
+
+
+def _kill(R):
+    p, conn = _SERVERS.pop(R)
+    p.kill()
+    p.join(timeout=30)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _stop_servers():
+    yield
+    for R in list(_SERVERS):
+        p, conn = _SERVERS[R]
+        try:
+            conn.send(None)
+            p.join(timeout=30)
+        except Exception:
+            pass
+        if p.is_alive():
+            p.kill()
+        _SERVERS.pop(R, None)
+
+
+def _threads(fn, R, *args):
+    p, conn = _server(R)
+    conn.send((fn, args))
+    if not conn.poll(_CALL_TIMEOUT_S):
+        _kill(R)
+        pytest.fail(f"{fn} at R={R} (co-resident): no result within {_CALL_TIMEOUT_S} s")
+    try:
+        out = conn.recv()
+    except EOFError:
+        _kill(R)
+        pytest.fail(f"{fn} at R={R} (co-resident): server died")
+    errors = [(r, v) for r, v in enumerate(out) if isinstance(v, str) and v.startswith("ERROR")]
+    if errors:
+        _kill(R)  # ranks may be stuck in a collective: start over
+        pytest.fail(f"rank {errors[0][0]}: {errors[0][1]}")
+    return dict(enumerate(out))
+
+
+def _run(layout, fn, *args):
+    mode, R = layout
+    return _threads(fn, R, *args) if mode == "thread" else _spawn(fn, R, *args)
+
+
+def _layouts(*thread_ranks, proc=True, proc_min=2, proc_max=4):
+    """pytest params: co-resident thread layouts (any GPU box) + the one-process-
+    per-GPU layout on a multi-GPU box."""
+    out = [pytest.param(("thread", r), id=f"thread{r}") for r in thread_ranks]
+    if proc:
+        n = min(_ngpus(), proc_max)
+        out.append(pytest.param(("proc", max(n, proc_min)), id="proc",
+                                marks=[pytest.mark.multigpu,
+                                       pytest.mark.skipif(n < proc_min, reason=f"needs >= {proc_min} GPUs")]))
+    return out
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+
+
+def _host_check(rank, R, m, seed, recv):
+    """Rank `rank`'s receive buffer, copied to the host, against the host
+    oracle's orc_alltoallv of the same matrix over the payload bytes."""
+    import ctypes
+    import numpy as np
+    from oracle import ref
+    lib = ref.cpu_lib()
+    sends = []
+    for s in range(R):
+        row = [m[s * R + d] for d in range(R)]
+        buf = np.zeros(max(sum(row), 1), dtype=np.uint8)
+        off = 0
+        for d in range(R):
+            lib.orc_fill(buf[off:].ctypes.data_as(ctypes.c_void_p), 0, row[d], seed, s, d)
+            off += row[d]
+        sends.append(buf)
+    want = [np.zeros(max(sum(m[s * R + d] for s in range(R)), 1), dtype=np.uint8) for d in range(R)]
+    mat = (ctypes.c_uint64 * (R * R))(*m)
+    lib.orc_alltoallv(R, mat, (ctypes.c_void_p * R)(*[b.ctypes.data for b in sends]),
+                      (ctypes.c_void_p * R)(*[w.ctypes.data for w in want]))
+    n = sum(m[s * R + rank] for s in range(R))
+    got = recv[:n].cpu().numpy()
+    return int((got != want[rank][:n]).sum())
+
+
+def _slots(comm):
+    cfg = comm.config()
+    return cfg.channels_per_peer * (cfg.p2p_buffer // cfg.pipe_chunk)
+
+
+def _rings_bounded(comm):
+    """Device-side bounded-buffer check of every staging ring this rank fed
+    since the last call (reference tests/acceptance.cpp:270-288: occupancy
+    <= S; and no slot claimed while its previous chunk was undrained)."""
+    st = comm.stats(reset=True)
+    return st["slot_double_claims"] == 0 and st["slot_max_occupancy"] <= _slots(comm)
+
+
+def _exchange_and_check(comm, rank, R, m, register, seed, register_send=False, host_check=True):
     from paper_2604_00317_b200 import comm as C
     sc, sd, rc, rd = C.packed_displs(m, R, rank)
     send = torch.empty(max(sum(sc), 16), dtype=torch.uint8, device="cuda")
@@ -77,14 +285,18 @@ def _exchange_and_check(comm, rank, R, m, register, seed, register_send=False):
     h = comm.register(recv) if register else None
     hs = comm.register(send) if register_send else None
     comm.alltoallv(send, sc, sd, recv, rc, rd)
-    torch.cuda.synchronize()
+    _sync()
     comm.check_async()
     bad = torch.zeros(1, dtype=torch.int64, device="cuda")
     for s in range(R):
         C.check_payload(recv[rd[s]:], 0, rc[s], seed, s, rank, bad)
     # bytes past the packed segments are untouched
     tail_ok = bool((recv[sum(rc):] == 0xEE).all()) if recv.numel() > sum(rc) else True
-    torch.cuda.synchronize()
+    _sync()
+    # rank 0's buffer on the host against the oracle's all-to-allv (bounded size)
+    if host_check and rank == 0 and sum(m) <= 512 * MiB:
+        tail_ok = tail_ok and _host_check(rank, R, m, seed, recv) == 0
+    tail_ok = tail_ok and _rings_bounded(comm)
     if h is not None:
         comm.deregister(h)
     if hs is not None:
@@ -160,7 +372,7 @@ def w_stress_back_to_back(comm, rank, R):
             comm.set_config(pull=pull)  # a config change is a (host-synchronizing) collective
         m, sc, sd, rc, rd, send, recvs, hs, hr, seed = pool[i]
         comm.alltoallv(send, sc, sd, recvs[j], rc, rd)
-    torch.cuda.synchronize()
+    _sync()
     comm.check_async()
     bad = torch.zeros(1, dtype=torch.int64, device="cuda")
     for (m, sc, sd, rc, rd, send, recvs, hs, hr, seed) in pool:
@@ -168,7 +380,7 @@ def w_stress_back_to_back(comm, rank, R):
             if any(pi == pool.index((m, sc, sd, rc, rd, send, recvs, hs, hr, seed)) and pj == j for pi, pj, _ in plan):
                 for s in range(R):
                     C.check_payload(recvs[j][rd[s]:], 0, rc[s], seed, s, rank, bad)
-    torch.cuda.synchronize()
+    _sync()
     for (m, sc, sd, rc, rd, send, recvs, hs, hr, seed) in pool:
         if hs is not None:
             comm.deregister(hs)
@@ -185,11 +397,11 @@ def w_sendrecv_ring(comm, rank, R):
     with C.group():
         comm.send(x, n, (rank + 1) % R)
         comm.recv(y, n, (rank - 1) % R)
-    torch.cuda.synchronize()
+    _sync()
     comm.check_async()
     bad = torch.zeros(1, dtype=torch.int64, device="cuda")
     C.check_payload(y, 0, n, 5, (rank - 1) % R, rank, bad)
-    torch.cuda.synchronize()
+    _sync()
     return int(bad.item())
 
 
@@ -217,7 +429,7 @@ def w_mismatch(comm, rank, R):
     sd, rd = [0] * R, [0] * R
     try:
         comm.alltoallv(x, sc, sd, y, rc, rd)
-        torch.cuda.synchronize()
+        _sync()
     except Exception as e:  # host-side detection is acceptable too
         return "raised: " + str(e)[:60]
     return comm.async_error()
@@ -240,7 +452,7 @@ def w_moe(comm, rank, R):
         recv_x, recv_e, h = disp.dispatch(x, ids)
         y = recv_x * (recv_e.to(torch.float32) + rank * disp.experts_per_rank + 1).unsqueeze(1)
         out = disp.combine(y, h, w)
-        torch.cuda.synchronize()
+        _sync()
         comm.check_async()
         ref = (x.unsqueeze(1) * (ids.to(torch.float32) + 1).unsqueeze(2) * w.unsqueeze(2)).sum(1)
         ok = torch.allclose(out, ref, rtol=1e-5, atol=1e-5)
@@ -260,26 +472,25 @@ def w_graph(comm, rank, R):
     recv = torch.zeros(sum(rc), dtype=torch.uint8, device="cuda")
     hs, hr = comm.register(send), comm.register(recv)
     comm.alltoallv(send, sc, sd, recv, rc, rd)  # warm-up: the schedule is cached before capture
-    torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        comm.alltoallv(send, sc, sd, recv, rc, rd)
+    _sync()
+    g = _capture(lambda: comm.alltoallv(send, sc, sd, recv, rc, rd))
+    _barrier()  # every rank captured before any rank replays
     bads = []
     for i in range(5):
         for d in range(R):
             C.fill_payload(send[sd[d]:], 0, sc[d], 200 + i, rank, d)
         recv.zero_()
-        torch.cuda.synchronize()
+        _sync()
         g.replay()
-        torch.cuda.synchronize()
+        _sync()
         bad = torch.zeros(1, dtype=torch.int64, device="cuda")
         for s in range(R):
             C.check_payload(recv[rd[s]:], 0, rc[s], 200 + i, s, rank, bad)
-        torch.cuda.synchronize()
+        _sync()
         bads.append(int(bad.item()))
     comm.check_async()
     comm.alltoallv(send, sc, sd, recv, rc, rd)  # eager launches keep working after replays
-    torch.cuda.synchronize()
+    _sync()
     comm.deregister(hs)
     comm.deregister(hr)
     return bads
@@ -314,16 +525,16 @@ def w_overtake(comm, rank, R, big, small):
             C.fill_payload(send[sd[d]:], 0, sc[d], 40 + i, rank, d)
         handles += [comm.register(send), comm.register(recv)]
         bufs.append((m, sc, sd, recv, rc, rd, send))
-    torch.cuda.synchronize()
+    _sync()
     for m, sc, sd, recv, rc, rd, send in bufs:  # no host sync between the launches
         comm.alltoallv(send, sc, sd, recv, rc, rd)
-    torch.cuda.synchronize()
+    _sync()
     comm.check_async()
     bad = torch.zeros(1, dtype=torch.int64, device="cuda")
     for i, (m, sc, sd, recv, rc, rd, send) in enumerate(bufs):
         for s in range(R):
             C.check_payload(recv[rd[s]:], 0, rc[s], 40 + i, s, rank, bad)
-    torch.cuda.synchronize()
+    _sync()
     for h in handles:
         comm.deregister(h)
     comm.set_config(pull=0)
@@ -354,10 +565,10 @@ def w_ll(comm, rank, R):
             for d in range(R):
                 C.fill_payload(send[sd[d]:], 0, sc[d], 60 + i, rank, d)
             runs.append((sc, sd, rc, rd, send, recv))
-        torch.cuda.synchronize()
+        _sync()
         for sc, sd, rc, rd, send, recv in runs:  # no host sync in between
             comm.alltoallv(send, sc, sd, recv, rc, rd)
-        torch.cuda.synchronize()
+        _sync()
         comm.check_async()
         bad = torch.zeros(1, dtype=torch.int64, device="cuda")
         for i, (sc, sd, rc, rd, send, recv) in enumerate(runs):
@@ -365,7 +576,7 @@ def w_ll(comm, rank, R):
                 C.check_payload(recv[rd[src]:], 0, rc[src], 60 + i, src, rank, bad)
             if recv.numel() > sum(rc):
                 bad += int((recv[sum(rc):] != 0xEE).sum())
-        torch.cuda.synchronize()
+        _sync()
         out.append(int(bad.item()))
     comm.set_config(ll_max=1 << 20)
     # an all-LL exchange captured in a CUDA graph
@@ -374,21 +585,20 @@ def w_ll(comm, rank, R):
     send = torch.empty(sum(sc), dtype=torch.uint8, device="cuda")
     recv = torch.zeros(sum(rc), dtype=torch.uint8, device="cuda")
     comm.alltoallv(send, sc, sd, recv, rc, rd)
-    torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        comm.alltoallv(send, sc, sd, recv, rc, rd)
+    _sync()
+    g = _capture(lambda: comm.alltoallv(send, sc, sd, recv, rc, rd))
+    _barrier()
     bad = torch.zeros(1, dtype=torch.int64, device="cuda")
     for i in range(4):
         for d in range(R):
             C.fill_payload(send[sd[d]:], 0, sc[d], 90 + i, rank, d)
         recv.zero_()
-        torch.cuda.synchronize()
+        _sync()
         g.replay()
-        torch.cuda.synchronize()
+        _sync()
         for src in range(R):
             C.check_payload(recv[rd[src]:], 0, rc[src], 90 + i, src, rank, bad)
-    torch.cuda.synchronize()
+    _sync()
     comm.check_async()
     out.append(int(bad.item()))
     return out
@@ -404,7 +614,7 @@ def w_ll_mismatch(comm, rank, R):
     rc = [n - (1 if rank == 1 and s == 0 else 0) if s != rank else 0 for s in range(R)]
     try:
         comm.alltoallv(x, sc, [0] * R, y, rc, [0] * R)
-        torch.cuda.synchronize()
+        _sync()
     except Exception as e:  # host-side detection is acceptable too
         return "raised: " + str(e)[:60]
     return comm.async_error()
@@ -426,10 +636,10 @@ def w_sendrecv_mixed(comm, rank, R):
             with C.group():
                 comm.send(x, n_out, 1 - rank)
                 comm.recv(y, n_in, 1 - rank)
-            torch.cuda.synchronize()
+            _sync()
             comm.check_async()
             C.check_payload(y, 0, n_in, 500 + it, 1 - rank, rank, bad)
-        torch.cuda.synchronize()
+        _sync()
         return int(bad.item())
     for it, (small, big) in enumerate([(3, 300001), (8192 + 5, 2 * MiB + 1), (262144, 262145)]):
         xs = torch.empty(small, dtype=torch.uint8, device="cuda")
@@ -447,11 +657,11 @@ def w_sendrecv_mixed(comm, rank, R):
             if R > 3:
                 comm.send(z, 0, (rank + 2) % R)
                 comm.recv(z, 0, (rank - 2) % R)
-        torch.cuda.synchronize()
+        _sync()
         comm.check_async()
         C.check_payload(ys, 0, small, 300 + it, left, rank, bad)
         C.check_payload(yb, 0, big, 400 + it, right, rank, bad)
-    torch.cuda.synchronize()
+    _sync()
     return int(bad.item())
 
 
@@ -473,7 +683,7 @@ def w_moe_autograd(comm, rank, R):
     y = recv_x * (recv_e.to(torch.float32) + rank * epr + 1).unsqueeze(1)
     out = moe.combine(comm, y, h, w)
     (out * gout).sum().backward()
-    torch.cuda.synchronize()
+    _sync()
     comm.check_async()
     x2, w2 = x.detach().clone().requires_grad_(True), w.detach().clone().requires_grad_(True)
     ref = (x2.unsqueeze(1) * (ids.to(torch.float32) + 1).unsqueeze(2) * w2.unsqueeze(2)).sum(1)
@@ -502,14 +712,14 @@ def w_stress_ll(comm, rank, R):
         recvs = [torch.zeros(max(sum(rc), 16), dtype=torch.uint8, device="cuda") for _ in range(2)]
         hs = [comm.register(send), comm.register(recvs[0])] if it != 1 else []
         pool.append((sc, sd, rc, rd, send, recvs, hs, 70 + it))
-    torch.cuda.synchronize()
+    _sync()
     plan = [(rng.randrange(3), rng.randrange(2)) for _ in range(40)]
     for k, (i, j) in enumerate(plan):
         if k % 10 == 0:
             comm.set_config(pull=rng.choice([0, 1, 2]))
         sc, sd, rc, rd, send, recvs, hs, seed = pool[i]
         comm.alltoallv(send, sc, sd, recvs[j], rc, rd)
-    torch.cuda.synchronize()
+    _sync()
     comm.check_async()
     bad = torch.zeros(1, dtype=torch.int64, device="cuda")
     for i, (sc, sd, rc, rd, send, recvs, hs, seed) in enumerate(pool):
@@ -517,7 +727,7 @@ def w_stress_ll(comm, rank, R):
             if (i, j) in plan:
                 for s in range(R):
                     C.check_payload(recvs[j][rd[s]:], 0, rc[s], seed, s, rank, bad)
-    torch.cuda.synchronize()
+    _sync()
     for (sc, sd, rc, rd, send, recvs, hs, seed) in pool:
         for h in hs:
             comm.deregister(h)
@@ -529,98 +739,177 @@ def w_bench(comm, rank, R):
     return comm.bench_skewed(32 * MiB, 0.7, 0, warmup=1, iters=3)
 
 
-need2 = pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
-need3 = pytest.mark.skipif(_ngpus() < 3, reason="needs >= 3 GPUs")
+def w_relay_split(comm, rank, R, nbytes):
+    """c1 / c2: p2p 0 -> 1 on the mesh model.  Delivery is checked byte for
+    byte, and the engine's per-kind device byte counters show the plan's
+    split really crossed the relays: rank 0 pushes the direct flow and stages
+    each relay flow into its relay's ring, every relay forwards exactly its
+    flow to rank 1 (reference test_planner.cpp:96-111
+    style goldens).  Also returns the slot-occupancy counters."""
+    from paper_2604_00317_b200 import planner as P
+    comm.set_config(fabric="alltoall", gpus_per_node=R)
+    comm.stats(reset=True)
+    m = P.gen_p2p(R, 0, 1, nbytes)
+    bad, ok = _exchange_and_check(comm, rank, R, m, True, 23, host_check=nbytes <= 256 * MiB)
+    st = comm.stats(reset=True)  # _exchange_and_check already read / reset the ring counters
+    comm.set_config(fabric="nvswitch")
+    return bad, ok, {k: st[k] for k in ("push", "stage", "forward", "pull", "drain")}
 
 
-@need2
+def w_check_detects_corruption(comm, rank, R):
+    """The device checker counts exactly the bytes an exchange got wrong."""
+    from paper_2604_00317_b200 import comm as C
+    from paper_2604_00317_b200 import planner as P
+    m = P.gen_skewed_a2av(R, 3 * MiB + 5, 0.7, 0)
+    sc, sd, rc, rd = C.packed_displs(m, R, rank)
+    send = torch.empty(max(sum(sc), 16), dtype=torch.uint8, device="cuda")
+    recv = torch.zeros(max(sum(rc), 16), dtype=torch.uint8, device="cuda")
+    for d in range(R):
+        C.fill_payload(send[sd[d]:], 0, sc[d], 3, rank, d)
+    comm.alltoallv(send, sc, sd, recv, rc, rd)
+    _sync()
+    src = (rank + 1) % R
+    flips = [0, 1, rc[src] // 2, rc[src] - 1]
+    for f in flips:
+        recv[rd[src] + f] ^= 0x5A
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for s in range(R):
+        C.check_payload(recv[rd[s]:], 0, rc[s], 3, s, rank, bad)
+    _sync()
+    return int(bad.item()), len(set(flips))
+
+
+ALL = _layouts(2, 4, 8)
+SOME = _layouts(2, 8)
+
+
+@pytest.mark.parametrize("layout", ALL)
 @pytest.mark.parametrize("register", [True, False])
 @pytest.mark.parametrize("per_rank,ratio", [(8 * MiB + 13, 0.7), (64 * MiB, 0.9), (1000, 0.5)])
-def test_skewed_alltoallv(per_rank, ratio, register):
-    R = min(_ngpus(), 4)
-    for r, (bad, tail_ok) in _spawn("w_skewed", R, per_rank, ratio, register).items():
-        assert bad == 0 and tail_ok, r
+def test_skewed_alltoallv(layout, per_rank, ratio, register):
+    for r, (bad, ok) in _run(layout, "w_skewed", per_rank, ratio, register).items():
+        assert bad == 0 and ok, r
 
 
-@need2
-def test_pull_modes_all_registration_combinations():
-    R = min(_ngpus(), 4)
-    for r, res in _spawn("w_pull_modes", R).items():
+@pytest.mark.parametrize("layout", ALL)
+def test_pull_modes_all_registration_combinations(layout):
+    for r, res in _run(layout, "w_pull_modes").items():
         assert all(bad == 0 and ok for bad, ok in res), (r, res)
 
 
-@need2
-def test_irregular_c4_sizes_registered_and_staged():
-    R = min(_ngpus(), 4)
-    for r, res in _spawn("w_irregular", R).items():
+@pytest.mark.parametrize("layout", ALL)
+def test_irregular_c4_sizes_registered_and_staged(layout):
+    for r, res in _run(layout, "w_irregular").items():
         assert all(bad == 0 and ok for bad, ok in res), (r, res)
 
 
-@need2
-def test_repeated_mixed_exchanges():
-    R = min(_ngpus(), 4)
-    for r, res in _spawn("w_repeat_mixed", R).items():
+@pytest.mark.parametrize("layout", SOME)
+def test_repeated_mixed_exchanges(layout):
+    for r, res in _run(layout, "w_repeat_mixed").items():
         assert all(bad == 0 and ok for bad, ok in res), (r, res)
 
 
-@need2
-def test_stress_back_to_back_exchanges():
-    R = min(_ngpus(), 4)
-    assert all(v == 0 for v in _spawn("w_stress_back_to_back", R).values())
+@pytest.mark.parametrize("layout", ALL)
+def test_stress_back_to_back_exchanges(layout):
+    assert all(v == 0 for v in _run(layout, "w_stress_back_to_back").values())
 
 
-@need2
-def test_sendrecv_group_ring():
-    R = min(_ngpus(), 4)
-    assert all(v == 0 for v in _spawn("w_sendrecv_ring", R).values())
+@pytest.mark.parametrize("layout", SOME)
+def test_sendrecv_group_ring(layout):
+    assert all(v == 0 for v in _run(layout, "w_sendrecv_ring").values())
 
 
-@need3
-def test_relay_routes_execute_bit_exact():
-    R = min(_ngpus(), 4)
-    for r, ((bad, ok), relays, mism) in _spawn("w_relay", R, 256 * MiB).items():
+@pytest.mark.parametrize("layout", _layouts(3, 4, proc_min=3))
+def test_relay_routes_execute_bit_exact(layout):
+    R = layout[1]
+    for r, ((bad, ok), relays, mism) in _run(layout, "w_relay", 256 * MiB).items():
         assert bad == 0 and ok and mism == 0, r
         assert relays == R - 2  # one relay flow per intermediate GPU (SURVEY.md sec. 8(a) row 10)
 
 
-@need2
-def test_count_mismatch_is_an_error_not_a_hang():
-    R = min(_ngpus(), 4)
-    res = _spawn("w_mismatch", R)
+C1_DIRECT, C1_RELAY = 33554432, 33554432                  # c1: 64 MiB on mesh3 (SURVEY.md sec. 8(a) row 10)
+C2_DIRECT, C2_RELAY = 360710144, 356515840                # c2: 1 GiB on mesh4: direct + 2 relays
+
+
+@pytest.mark.parametrize("layout", _layouts(3, proc_min=3, proc_max=3))
+def test_c1_relay_split_crosses_the_relay(layout):
+    out = _run(layout, "w_relay_split", 64 * MiB)
+    for r, (bad, ok, st) in out.items():
+        assert bad == 0 and ok, r
+    st0, st2 = out[0][2], out[2][2]
+    assert st0["push"][1] == C1_DIRECT and st0["stage"][2] == C1_RELAY and st0["pull"] == [0, 0, 0]
+    assert st2["forward"][1] == C1_RELAY and sum(st2["push"]) == 0
+    assert sum(out[1][2]["push"]) + sum(out[1][2]["stage"]) == 0  # rank 1 only receives
+
+
+@pytest.mark.parametrize("layout", _layouts(4, proc_min=4, proc_max=4))
+def test_c2_two_relays_split(layout):
+    out = _run(layout, "w_relay_split", 1 << 30)
+    for r, (bad, ok, st) in out.items():
+        assert bad == 0 and ok, r
+    st0 = out[0][2]
+    assert st0["push"][1] == C2_DIRECT and st0["stage"][2] == C2_RELAY and st0["stage"][3] == C2_RELAY
+    for v in (2, 3):
+        assert out[v][2]["forward"][1] == C2_RELAY, v
+    assert C2_DIRECT + 2 * C2_RELAY == 1 << 30
+
+
+@pytest.mark.parametrize("layout", SOME)
+def test_checker_counts_corrupted_bytes(layout):
+    for r, (bad, want) in _run(layout, "w_check_detects_corruption").items():
+        assert bad == want, (r, bad, want)
+
+
+@pytest.mark.parametrize("layout", SOME)
+def test_count_mismatch_is_an_error_not_a_hang(layout):
+    res = _run(layout, "w_mismatch")
     assert any(v not in (0, "0") for v in res.values()), res
 
 
-@need2
-def test_moe_dispatch_combine():
-    R = min(_ngpus(), 4)
-    res = _spawn("w_moe", R)
+@pytest.mark.parametrize("layout", _layouts(2, 4))
+def test_moe_dispatch_combine(layout):
+    res = _run(layout, "w_moe")
     assert all(ok for ok, _ in res.values()), res
     assert res[0][1] > max(n for r, (_, n) in res.items() if r != 0)  # rank 0 holds the hot expert
 
 
-@need2
-def test_cuda_graph_capture_and_replay():
-    R = min(_ngpus(), 4)
-    for r, bads in _spawn("w_graph", R).items():
+@pytest.mark.parametrize("layout", ALL)
+def test_cuda_graph_capture_and_replay(layout):
+    for r, bads in _run(layout, "w_graph").items():
         assert bads == [0] * 5, (r, bads)
 
 
-@need2
-def test_bench_entry_point():
-    R = min(_ngpus(), 4)
-    for r, b in _spawn("w_bench", R).items():
+@pytest.mark.parametrize("layout", SOME)
+def test_bench_entry_point(layout):
+    for r, b in _run(layout, "w_bench").items():
         assert b["mismatches"] == 0 and b["gbps_effective"] > 0 and b["bound_seconds"] > 0
 
 
-@need2
+@pytest.mark.multigpu
+@pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
 def test_comm_init_all_single_process_grouped():
     """nimbleCommInitAll: every GPU in this process, one grouped call per step
     (NCCL's single-process pattern), registered and unregistered receives,
     mesh model (row allgather inside the clique) included."""
+    _init_all_grouped(list(range(min(_ngpus(), 4))))
+
+
+@pytest.mark.parametrize("R", [2, 4])
+def test_comm_init_all_repeated_device(R):
+    """nimbleCommInitAll([0] * R): R co-resident ranks driven from ONE thread
+    with grouped calls, one stream per rank."""
+    _init_all_grouped([0] * R)
+
+
+def _init_all_grouped(devices):
     from paper_2604_00317_b200 import comm as C
     from paper_2604_00317_b200 import planner as P
-    R = min(_ngpus(), 4)
-    comms = C.Comm.init_all(list(range(R)))
+    R = len(devices)
+    comms = C.Comm.init_all(devices)
+    streams = []
+    for c in comms:
+        with torch.cuda.device(c.device):
+            streams.append(torch.cuda.Stream())
     try:
         for fabric, register, per_rank in (("nvswitch", True, 3 * MiB + 1), ("nvswitch", False, 3 * MiB + 1),
                                            ("alltoall", True, 0), ("nvswitch", False, 100 * 1024 + 3)):  # last: LL
@@ -640,12 +929,12 @@ def test_comm_init_all_single_process_grouped():
                     hs = [c.register(send), c.register(recv)] if register else []
                     bufs.append((c, send, recv, sc, sd, rc, rd, hs))
             with C.group():
-                for c, send, recv, sc, sd, rc, rd, hs in bufs:
+                for (c, send, recv, sc, sd, rc, rd, hs), st in zip(bufs, streams):
                     with torch.cuda.device(c.device):
-                        c.alltoallv(send, sc, sd, recv, rc, rd)
-            for c, send, recv, sc, sd, rc, rd, hs in bufs:
+                        c.alltoallv(send, sc, sd, recv, rc, rd, stream=st)
+            for (c, send, recv, sc, sd, rc, rd, hs), st in zip(bufs, streams):
                 with torch.cuda.device(c.device):
-                    torch.cuda.synchronize()
+                    st.synchronize()
                     c.check_async()
                     bad = torch.zeros(1, dtype=torch.int64, device="cuda")
                     for s in range(R):
@@ -660,42 +949,38 @@ def test_comm_init_all_single_process_grouped():
                 c.destroy()
 
 
-@need2
+@pytest.mark.parametrize("layout", _layouts(2, proc_max=2))
 @pytest.mark.parametrize("small", [(1 << 20) + 300 * 1024 + 3, 4096 + 3])  # pull path (> ll_max), LL path
-def test_receiver_two_launches_ahead_of_sender(small):
-    out = _spawn("w_overtake", 2, 4 << 30, small)
+def test_receiver_two_launches_ahead_of_sender(layout, small):
+    out = _run(layout, "w_overtake", 4 << 30, small)
     assert all(v == 0 for v in out.values()), out
 
 
-@need2
-def test_low_latency_protocol_small_pairs():
-    R = min(_ngpus(), 4)
-    out = _spawn("w_ll", R)
+@pytest.mark.parametrize("layout", ALL)
+def test_low_latency_protocol_small_pairs(layout):
+    out = _run(layout, "w_ll")
     assert all(v == [0, 0, 0, 0] for v in out.values()), out  # three ll_max settings + the graph
 
 
-@need2
-def test_low_latency_size_mismatch_is_an_error():
-    out = _spawn("w_ll_mismatch", 2)
+@pytest.mark.parametrize("layout", _layouts(2, proc_max=2))
+def test_low_latency_size_mismatch_is_an_error(layout):
+    out = _run(layout, "w_ll_mismatch")
     assert out[1] != 0, out  # the receiver that expected fewer bytes reports it
 
 
-@need2
-def test_sendrecv_group_mixed_sizes_and_peers():
-    R = min(_ngpus(), 4)
-    out = _spawn("w_sendrecv_mixed", R)
+@pytest.mark.parametrize("layout", _layouts(2, 3, 8))
+def test_sendrecv_group_mixed_sizes_and_peers(layout):
+    out = _run(layout, "w_sendrecv_mixed")
     assert all(v == 0 for v in out.values()), out
 
 
-@need2
-def test_moe_custom_op_forward_and_gradients():
-    R = min(_ngpus(), 4)
-    res = _spawn("w_moe_autograd", R)
+@pytest.mark.parametrize("layout", _layouts(2, 4))
+def test_moe_custom_op_forward_and_gradients(layout):
+    res = _run(layout, "w_moe_autograd")
     assert all(ok for ok, _ in res.values()), res
 
 
-@need2
-def test_stress_ll_and_normal_pairs_back_to_back():
-    R = min(_ngpus(), 4)
-    out = _spawn("w_stress_ll", R)
+@pytest.mark.parametrize("layout", ALL)
+def test_stress_ll_and_normal_pairs_back_to_back(layout):
+    out = _run(layout, "w_stress_ll")
     assert all(v == 0 for v in out.values()), out
