@@ -50,6 +50,39 @@ def workload_matrix(R, per_rank, ratio, hot=0):
     return P.gen_skewed_a2av(R, per_rank, ratio, hot)
 
 
+def reference_matrix(R, per_rank, ratio, hot=0):
+    """The same matrix from the reference's own generator (oracle/_ref,
+    proj/src/workloads.cpp:66-92), or the oracle's restatement of it when the
+    reference was not compiled -- the reference arm loads no product code."""
+    from oracle import ref
+    if ref.available():
+        req = {"op": "gen", "ranks": R, "workload": {"kind": "skewed", "size": per_rank, "ratio": ratio, "hot": hot}}
+        return [int(x) for x in ref.call(req)["matrix"]]
+    from oracle import nimble_oracle as O
+    return list(O.gen_skewed_a2av(R, per_rank, ratio, hot).bytes)
+
+
+def config_of(R, args):
+    """The workload, identical in both arms' JSON lines."""
+    per_rank = args.per_rank_mib * MiB
+    cfg = {"workload": f"c3 skewed all-to-allv, {R} ranks, {args.per_rank_mib} MiB/rank, hotspot ratio "
+                       f"{args.ratio}, hot rank 0" + (", new counts every step" if args.fresh_matrix else ""),
+           "ranks": R, "per_rank_bytes": per_rank, "ratio": args.ratio}
+    return cfg
+
+
+def fresh_matrices(base, R, k, seed=12345):
+    """k distinct count matrices near `base` (every entry lowered by a seeded
+    0-1% so the buffers sized for `base` hold them all): the counts change
+    every step, as a MoE dispatch's do.  Same on every rank."""
+    import random
+    rng = random.Random(seed)
+    out = []
+    for _ in range(k):
+        out.append([0 if v == 0 else v - rng.randrange(v // 100 + 1) for v in base])
+    return out
+
+
 def max_over_ranks(x: float) -> float:
     import torch
     import torch.distributed as dist
@@ -224,6 +257,9 @@ def cpu_baseline(R, m, max_seconds=20.0):
     n = len(src)
     arr = lambda t, v: (t * max(n, 1))(*v)  # noqa: E731
     total = sum(m)
+    # one untimed rep: page in the host buffers
+    cpu.orc_exchange_flows(R, mat, sp, rp, n, arr(ctypes.c_int, src), arr(ctypes.c_int, dst),
+                           arr(ctypes.c_int, via), arr(ctypes.c_double, byt), None, 1 << 20, cores)
     reps, spent = 0, 0.0
     while reps < 1 or (spent < max_seconds and reps < 20):
         t0 = time.perf_counter()
@@ -256,23 +292,33 @@ def run_local(args):
         for d in range(R):
             C.fill_payload(sends[s][sd[d]:], 0, sc[d], 1, s, d)
     stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
-        C.exchange_local(sends, recvs, m, args.ctas, stream)
+    # --fresh-matrix: every step brings new counts (MoE-style); the schedule is
+    # generated on the device per step (nimbleExchangeLocal keeps 4 entries,
+    # and the steps cycle through more matrices than that)
+    mats = fresh_matrices(m, R, args.steps + args.warmup) if args.fresh_matrix else None
+    step_m = (lambda k: mats[k]) if mats else (lambda k: m)
+    for k in range(args.warmup):
+        C.exchange_local(sends, recvs, step_m(args.steps + k) if mats else m, args.ctas, stream)
     torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    host_s = []
     with Clocks(0) as clk:
         torch.cuda.synchronize()
         ev[0].record(stream)
         for k in range(args.steps):
-            C.exchange_local(sends, recvs, m, args.ctas, stream)
+            t0 = time.perf_counter()
+            C.exchange_local(sends, recvs, step_m(k), args.ctas, stream)
+            host_s.append(time.perf_counter() - t0)
             ev[k + 1].record(stream)
         torch.cuda.synchronize()
     per_step = [ev[k].elapsed_time(ev[k + 1]) * 1e-3 for k in range(args.steps)]
     t_total = ev[0].elapsed_time(ev[-1]) * 1e-3
+    moved = sum(sum(step_m(k)) for k in range(args.steps))
     # verify the last step's delivery
+    last = step_m(args.steps - 1)
     bad = torch.zeros(1, dtype=torch.int64, device="cuda")
     for d in range(R):
-        _, _, rc, rd = C.packed_displs(m, R, d)
+        _, _, rc, rd = C.packed_displs(last, R, d)
         for s in range(R):
             C.check_payload(recvs[d][rd[s]:], 0, rc[s], 1, s, d, bad)
     mismatches = int(bad.item())
@@ -316,23 +362,25 @@ def run_local(args):
 
     peak, peak_src = measured_peaks()
     kernel_s = sum(per_step) / len(per_step)
-    achieved = 2 * total / kernel_s / 1e9
+    achieved = 2 * moved / args.steps / kernel_s / 1e9
     line = {
-        "metric": METRIC, "value": total * args.steps / t_total / 1e9, "unit": "GB/s", "n_gpus": 1,
+        "metric": METRIC, "value": moved / t_total / 1e9, "unit": "GB/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_total / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic: gen_skewed_a2av matrix, splitmix64 payload bytes (seed 1)",
-        "config": {"workload": f"c3 skewed all-to-allv, {R} ranks emulated on 1 GPU (local-copy calibration), "
-                               f"{args.per_rank_mib} MiB/rank, hotspot ratio {ratio}, hot rank 0",
-                   "ranks": R, "per_rank_bytes": per_rank, "ratio": ratio, "total_bytes": total,
-                   "layout": "packed MPI all-to-allv (misaligned segments)",
-                   "l2": f"inputs {total / 2**30:.2f} GiB > 126 MB L2, no flush"},
+        "config": config_of(R, args),
+        "setup": {"ranks_on_gpu": f"all {R} ranks' buffers on 1 GPU, one engine launch per step (local-copy "
+                                  "calibration of the data path)",
+                  "total_bytes": total, "layout": "packed MPI all-to-allv (misaligned segments)",
+                  "l2": f"inputs {total / 2**30:.2f} GiB > 126 MB L2, no flush",
+                  "host_us_per_call": statistics.median(host_s) * 1e6,
+                  "schedule": "generated on the device per new matrix" if mats else "cached (same matrix every step)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _ncu_traffic("local"),
                      "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)",
-                     "algorithmic_bytes_per_launch": 2 * total, "kernel": "nb::exchange_kernel"},
+                     "algorithmic_bytes_per_launch": 2 * moved // args.steps, "kernel": "nb::exchange_kernel"},
         "verified": {"mismatched_bytes": mismatches},
-        "gpu_launches": args.steps,
+        "gpu_launches": args.steps * (2 if mats else 1),
         "clocks": clk.summary(),
         "e2e": e2e,
         "baselines": {"torch_copy_gbps": torch_gbps},
@@ -381,25 +429,38 @@ def run_multi(args):
     handle = comm.register(recv)
     shandle = comm.register(send)  # lets ingress-heavy receivers pull (receiver-driven TMA loads)
     stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
-        comm.alltoallv(send, sc, sd, recv, rc, rd, stream)
+    # --fresh-matrix: new counts every step (plan + schedule + launch per call,
+    # all inside the timed region); otherwise the same matrix every step
+    mats = fresh_matrices(m, R, args.steps + args.warmup) if args.fresh_matrix else None
+    layouts = [C.packed_displs(x, R, rank) for x in mats] if mats else None
+    lay = (lambda k: layouts[k]) if mats else (lambda k: (sc, sd, rc, rd))
+    for k in range(args.warmup):
+        a, b, c_, d_ = lay(args.steps + k) if mats else lay(0)
+        comm.alltoallv(send, a, b, recv, c_, d_, stream)
     torch.cuda.synchronize()
     comm.check_async()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    host_s = []
     with Clocks(local) as clk:
         barrier()
         torch.cuda.synchronize()
         e0.record(stream)
-        for _ in range(args.steps):
-            comm.alltoallv(send, sc, sd, recv, rc, rd, stream)
+        for k in range(args.steps):
+            a, b, c_, d_ = lay(k)
+            t0 = time.perf_counter()
+            comm.alltoallv(send, a, b, recv, c_, d_, stream)
+            host_s.append(time.perf_counter() - t0)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
     t = max_over_ranks(e0.elapsed_time(e1) * 1e-3)
+    host_us = max_over_ranks(statistics.median(host_s) * 1e6)
+    moved = sum(sum(mats[k]) for k in range(args.steps)) if mats else total * args.steps
     comm.check_async()
+    _, _, lrc, lrd = lay(args.steps - 1)
     bad = torch.zeros(1, dtype=torch.int64, device="cuda")
     for s in range(R):
-        C.check_payload(recv[rd[s]:], 0, rc[s], 1, s, rank, bad)
+        C.check_payload(recv[lrd[s]:], 0, lrc[s], 1, s, rank, bad)
     torch.cuda.synchronize()
     mismatches = int(max_over_ranks(float(bad.item())))
 
@@ -446,26 +507,30 @@ def run_multi(args):
 
     comm.deregister(handle)
     comm.deregister(shandle)
-    bound_s = port_bytes(m, R) / (PORT_GBPS * 1e9)
+    port = (sum(port_bytes(mats[k], R) for k in range(args.steps)) // args.steps) if mats else port_bytes(m, R)
+    bound_s = port / (PORT_GBPS * 1e9)
     step_s = t / args.steps
-    achieved = port_bytes(m, R) / step_s / 1e9
+    achieved = port / step_s / 1e9
     line = {
-        "metric": METRIC, "value": total * args.steps / t / 1e9, "unit": "GB/s", "n_gpus": world,
+        "metric": METRIC, "value": moved / t / 1e9, "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic: gen_skewed_a2av matrix, splitmix64 payload bytes (seed 1)",
-        "config": {"workload": f"skewed all-to-allv, {R} ranks (1 per GPU, NVLink), {args.per_rank_mib} MiB/rank, "
-                               f"hotspot ratio {ratio}, hot rank 0",
-                   "ranks": R, "per_rank_bytes": per_rank, "ratio": ratio, "total_bytes": total,
-                   "parallelism": f"{R} ranks", "receive": "registered send + receive windows (zero copy; ingress-heavy ranks pull)",
-                   "l2": "per-rank inputs >= 256 MiB > 126 MB L2, no flush"},
+        "config": config_of(R, args),
+        "setup": {"ranks_on_gpu": f"{R} ranks, 1 per GPU (NVLink)", "total_bytes": total,
+                  "parallelism": f"{R} ranks",
+                  "receive": "registered send + receive windows (zero copy; ingress-heavy ranks pull)",
+                  "l2": "per-rank inputs >= 256 MiB > 126 MB L2, no flush",
+                  "host_us_per_call": host_us,
+                  "schedule": "planned + generated on the device per new matrix" if mats
+                              else "cached (same matrix every step)"},
         "roofline": {"bound": "nvlink_port", "achieved": achieved, "peak": PORT_GBPS, "unit": "GB/s",
-                     "frac": achieved / PORT_GBPS, "traffic": None, "bound_ms": bound_s * 1e3,
+                     "frac": achieved / PORT_GBPS, "traffic": _ncu_traffic(f"n{R}"), "bound_ms": bound_s * 1e3,
                      "peak_source": "nominal NVLink-5 port, 900 GB/s per direction (north star); "
                                     "measured peer copy 770 GB/s (B200_PROFILING.md)",
-                     "algorithmic_bytes_per_launch": port_bytes(m, R), "kernel": "nb::exchange_kernel"},
+                     "algorithmic_bytes_per_launch": port, "kernel": "nb::exchange_kernel"},
         "verified": {"mismatched_bytes": mismatches},
-        "gpu_launches": args.steps,
+        "gpu_launches": args.steps * (2 if mats else 1),
         "clocks": clk.summary(),
         "e2e": e2e,
         "baselines": {"nccl": nccl},
@@ -484,14 +549,14 @@ def run_reference(args):
     if rank != 0:
         return None
     R = 8 if world == 1 else world
-    m = workload_matrix(R, args.per_rank_mib * MiB, args.ratio)
+    m = reference_matrix(R, args.per_rank_mib * MiB, args.ratio)
     v, cores, kind, sample, model = cpu_baseline(R, m, args.cpu_seconds)
     return {
         "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": sum(m) / (v * 1e9) * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "u8", "data": "synthetic: gen_skewed_a2av matrix", "impl": "reference",
-        "config": {"workload": f"skewed all-to-allv, {R} ranks, {args.per_rank_mib} MiB/rank, hotspot ratio "
-                               f"{args.ratio}", "ranks": R, "total_bytes": sum(m)},
+        "dtype": "u8", "data": "synthetic: gen_skewed_a2av matrix (the reference's generator)", "impl": "reference",
+        "config": config_of(R, args),
+        "setup": {"total_bytes": sum(m), "ranks_on_gpu": "none: the reference's CPU path on the host cores"},
         "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": kind, "sample": sample,
                          "reference_model_gbps": model},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -517,6 +582,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-baselines", action="store_true")
+    ap.add_argument("--fresh-matrix", action="store_true",
+                    help="new counts every step: plan + schedule + launch per call inside the timed region")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

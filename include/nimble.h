@@ -318,6 +318,16 @@ nimbleResult_t nimbleDebugSchedule(nimblePlan_t plan, int rank, int ranks, uint6
                                    uint64_t pull_mask,
                                    nimbleItem* items, int cap, int* nitems);
 
+/* The same item list produced by the device-side generator (engine.cu,
+ * gen_items_kernel) on the current CUDA device: the flows go to the GPU as
+ * kernel parameters and are merged there -- how a communicator schedules a
+ * new matrix without a host merge or an upload.  Must equal
+ * nimbleDebugSchedule's list item for item. */
+nimbleResult_t nimbleDebugScheduleDevice(nimblePlan_t plan, int rank, int ranks, uint64_t pipe_chunk,
+                                         uint32_t slots, uint64_t direct_chunk, uint64_t push_chunk,
+                                         uint64_t recv_staged_mask, uint64_t pull_mask,
+                                         nimbleItem* items, int cap, int* nitems);
+
 /* Device timeline of the comm's last launch (%globaltimer ns): kernel start,
  * prologue done, first item, last item, CTAs done, completions signalled,
  * completions observed, first CTA done, latest work loops done, latest

@@ -131,6 +131,8 @@ SIGNATURES = {
     "nimbleCommGetStats": [c_void_p, P(CommStats), c_int],
     "nimbleDebugSchedule": [c_void_p, c_int, c_int, c_u64, ctypes.c_uint32, c_u64, c_u64, c_u64, c_u64, c_void_p, c_int,
                             P(c_int)],
+    "nimbleDebugScheduleDevice": [c_void_p, c_int, c_int, c_u64, ctypes.c_uint32, c_u64, c_u64, c_u64, c_u64, c_void_p,
+                                  c_int, P(c_int)],
 }
 _RESTYPES = {"nimbleGetErrorString": c_char_p, "nimbleGetLastError": c_char_p}
 

@@ -1,3 +1,4 @@
+#include <cuda_runtime.h>
 // C ABI, group 1: link-load model, traffic-matrix ingest, planner.
 // Host-only; exceptions from the C++ core become result codes here.
 #include <algorithm>
@@ -11,6 +12,7 @@
 #include "demand.hpp"
 #include "fabric.hpp"
 #include "planner.hpp"
+#include "device.cuh"
 #include "schedule.hpp"
 
 struct nimbleTopology {
@@ -353,43 +355,94 @@ nimbleResult_t nimblePlanToJson(nimblePlan_t p, char* out, size_t cap, size_t* n
     return nb::write_text(nb::plan_json(p->plan), out, cap, need);
 }
 
+}  // extern "C"
+
+namespace nb {
+cudaError_t launch_gen(const GenArgs& g, cudaStream_t st);
+namespace {
+
+// nimbleDebugSchedule's rank buffers: synthetic addresses, packed layout.
+Schedule debug_schedule(nimblePlan_t p, int rank, int ranks, uint64_t pipe_chunk, uint32_t slots,
+                        uint64_t direct_chunk, uint64_t push_chunk, uint64_t staged, uint64_t pull) {
+    if (!p || ranks < 1 || ranks > kMaxRanks || rank < 0 || rank >= ranks)
+        throw std::invalid_argument("schedule: bad argument");
+    std::vector<uint64_t> m(static_cast<size_t>(ranks) * ranks, 0);
+    for (const PairRoutes& pr : p->plan.pairs) m[static_cast<size_t>(pr.src) * ranks + pr.dst] = pr.demand;
+    RankBuffers rb;
+    rb.R = ranks;
+    rb.me = rank;
+    rb.send_ptr.assign(ranks, 0);
+    rb.send_bytes.assign(ranks, 0);
+    rb.recv_ptr.assign(ranks, 0);
+    rb.recv_bytes.assign(ranks, 0);
+    rb.recv_post.assign(ranks, Post{});
+    rb.send_post.assign(ranks, Post{});
+    uint64_t so = 0, ro = 0;
+    for (int q = 0; q < ranks; ++q) {
+        rb.send_bytes[q] = m[static_cast<size_t>(rank) * ranks + q];
+        rb.send_ptr[q] = (static_cast<uint64_t>(1 + rank) << 40) + so;
+        so += rb.send_bytes[q];
+        rb.recv_bytes[q] = m[static_cast<size_t>(q) * ranks + rank];
+        rb.recv_ptr[q] = (static_cast<uint64_t>(17 + rank) << 40) + ro;
+        ro += rb.recv_bytes[q];
+        if (q != rank && rb.recv_bytes[q]) {
+            Post& post = rb.recv_post[q];
+            post.tag = 1;
+            post.bytes = rb.recv_bytes[q];
+            post.mode = ((staged >> q) & 1) ? kPostStaged : kPostZeroCopy;
+            if ((pull >> q) & 1) post.mode |= kPostPullRequest;
+        }
+    }
+    return build_schedule(p->plan, rb, pipe_chunk, slots, direct_chunk, push_chunk);
+}
+
+}  // namespace
+}  // namespace nb
+
+extern "C" {
+
 nimbleResult_t nimbleDebugSchedule(nimblePlan_t p, int rank, int ranks, uint64_t pipe_chunk, uint32_t slots,
                                    uint64_t direct_chunk, uint64_t push_chunk, uint64_t staged, uint64_t pull,
                                    nimbleItem* items, int cap, int* nitems) {
     static_assert(sizeof(nimbleItem) == sizeof(nb::Item), "nimbleItem mirrors the engine's Item");
     return nb::guarded([&] {
-        if (!p || !nitems || ranks < 1 || ranks > nb::kMaxRanks || rank < 0 || rank >= ranks)
-            throw std::invalid_argument("schedule: bad argument");
-        std::vector<uint64_t> m(static_cast<size_t>(ranks) * ranks, 0);
-        for (const nb::PairRoutes& pr : p->plan.pairs) m[static_cast<size_t>(pr.src) * ranks + pr.dst] = pr.demand;
-        nb::RankBuffers rb;
-        rb.R = ranks;
-        rb.me = rank;
-        rb.send_ptr.assign(ranks, 0);
-        rb.send_bytes.assign(ranks, 0);
-        rb.recv_ptr.assign(ranks, 0);
-        rb.recv_bytes.assign(ranks, 0);
-        rb.recv_post.assign(ranks, nb::Post{});
-        rb.send_post.assign(ranks, nb::Post{});
-        uint64_t so = 0, ro = 0;
-        for (int q = 0; q < ranks; ++q) {
-            rb.send_bytes[q] = m[static_cast<size_t>(rank) * ranks + q];
-            rb.send_ptr[q] = (static_cast<uint64_t>(1 + rank) << 40) + so;
-            so += rb.send_bytes[q];
-            rb.recv_bytes[q] = m[static_cast<size_t>(q) * ranks + rank];
-            rb.recv_ptr[q] = (static_cast<uint64_t>(17 + rank) << 40) + ro;
-            ro += rb.recv_bytes[q];
-            if (q != rank && rb.recv_bytes[q]) {
-                nb::Post& post = rb.recv_post[q];
-                post.tag = 1;
-                post.bytes = rb.recv_bytes[q];
-                post.mode = ((staged >> q) & 1) ? nb::kPostStaged : nb::kPostZeroCopy;
-                if ((pull >> q) & 1) post.mode |= nb::kPostPullRequest;
-            }
-        }
-        nb::Schedule sc = nb::build_schedule(p->plan, rb, pipe_chunk, slots, direct_chunk, push_chunk);
+        if (!nitems) throw std::invalid_argument("schedule: bad argument");
+        nb::Schedule sc = nb::debug_schedule(p, rank, ranks, pipe_chunk, slots, direct_chunk, push_chunk, staged, pull);
+        nb::materialize(sc);
         *nitems = static_cast<int>(sc.items.size());
         if (items) std::memcpy(items, sc.items.data(), std::min<size_t>(sc.items.size(), cap > 0 ? cap : 0) * sizeof(nb::Item));
+    });
+}
+
+nimbleResult_t nimbleDebugScheduleDevice(nimblePlan_t p, int rank, int ranks, uint64_t pipe_chunk, uint32_t slots,
+                                         uint64_t direct_chunk, uint64_t push_chunk, uint64_t staged, uint64_t pull,
+                                         nimbleItem* items, int cap, int* nitems) {
+    return nb::guarded([&] {
+        if (!nitems) throw std::invalid_argument("schedule: bad argument");
+        nb::Schedule sc = nb::debug_schedule(p, rank, ranks, pipe_chunk, slots, direct_chunk, push_chunk, staged, pull);
+        if (sc.cuts.size() + sc.ll_cuts.size() > static_cast<size_t>(nb::kMaxGenCuts))
+            throw nb::Error(nimbleInvalidUsage, "schedule: more flows than the device generator takes");
+        *nitems = static_cast<int>(sc.nitems);
+        if (!items) return;
+        auto check = [](cudaError_t e) {
+            if (e != cudaSuccess) throw nb::Error(nimbleUnhandledCudaError, cudaGetErrorString(e));
+        };
+        nb::GenArgs g;
+        std::memset(&g, 0, sizeof g);
+        g.ncuts = g.nkeyed = static_cast<uint32_t>(sc.cuts.size());
+        g.nitems = sc.nitems;
+        std::copy(sc.cuts.begin(), sc.cuts.end(), g.cuts);
+        nb::Item* d = nullptr;
+        check(cudaMalloc(&d, std::max<size_t>(sc.nitems, 1) * sizeof(nb::Item)));
+        check(cudaMemset(d, 0xff, std::max<size_t>(sc.nitems, 1) * sizeof(nb::Item)));
+        g.items = d;
+        cudaError_t e = nb::launch_gen(g, nullptr);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        if (e == cudaSuccess)
+            e = cudaMemcpy(items, d, std::min<size_t>(sc.nitems, cap > 0 ? cap : 0) * sizeof(nb::Item),
+                           cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        check(e);
     });
 }
 

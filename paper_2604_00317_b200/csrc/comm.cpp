@@ -36,7 +36,8 @@
 #include "schedule.hpp"
 
 namespace nb {
-cudaError_t launch_exchange(const LaunchArgs& args, int ctas, cudaStream_t stream);
+cudaError_t launch_exchange(const LaunchArgs& args, int ctas, cudaStream_t stream, bool pdl = true);
+cudaError_t launch_gen(const GenArgs& g, cudaStream_t st);
 cudaError_t launch_fill(void* buf, uint64_t first, uint64_t n, uint64_t seed, int s, int d, cudaStream_t st);
 cudaError_t launch_check(const void* buf, uint64_t first, uint64_t n, uint64_t seed, int s, int d, uint64_t* bad,
                          cudaStream_t st);
@@ -142,6 +143,14 @@ struct DevBuf {
             n = v.size();
         }
         if (!v.empty()) CUDA_TRY(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+    }
+    // room for at least m elements (contents undefined)
+    void reserve(size_t m, cudaStream_t st) {
+        if (m <= n && p) return;
+        if (p) CUDA_TRY(cudaFreeAsync(p, st));
+        p = nullptr;
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(m, 1) * sizeof(T), st));
+        n = std::max<size_t>(m, 1);
     }
     void release() {
         if (p) cudaFreeAsync(p, cudaStreamPerThread);
@@ -388,10 +397,13 @@ void enable_peer(int dev) {
 // Default CTAs per launch.  A device hosting k ranks of this comm (one
 // process, k streams) runs k engine grids at once, and each grid's producers
 // spin on flags raised by the others: all of them must be resident together,
-// so each takes (SMs - k) / k CTAs -- one SM per rank to spare for the next
-// stream-ordered grid's early CTAs and any other kernel on the device.
+// and the kernels each rank runs between its exchanges (on its own stream,
+// possibly with large shared-memory footprints) must still find SMs while
+// the other ranks' grids spin.  So each grid takes SMs / 2k CTAs, and the
+// grids are launched without programmatic dependent launch (a grid whose
+// successor is pre-launched would hold twice its share).
 void set_share(nimbleComm* c) {
-    c->sms_share = c->colocated <= 1 ? c->sms : std::max(1, (c->sms - c->colocated) / c->colocated);
+    c->sms_share = c->colocated <= 1 ? c->sms : std::max(1, c->sms / (2 * c->colocated));
 }
 
 // Allocate ctrl + staging, exchange handles / pointers, map peers.
@@ -683,6 +695,32 @@ void fill_posts(nimbleComm* c, RankBuffers& rb, const PlanResult& plan) {
 constexpr size_t kCachedSchedules = 4;
 void reap_retired(nimbleComm* c);
 
+// Schedules whose flows fit the generator's parameter block are merged on
+// the device (NIMBLE_HOST_SCHEDULE=1 forces the host merge + upload).
+bool gen_on_device(const Schedule& sc) {
+    static const bool host = [] {
+        const char* e = std::getenv("NIMBLE_HOST_SCHEDULE");
+        return e && *e == '1';
+    }();
+    return !host && sc.cuts.size() + sc.ll_cuts.size() <= static_cast<size_t>(kMaxGenCuts);
+}
+
+void fill_gen(GenArgs& g, const Schedule& sc, int R) {
+    g.ncuts = static_cast<uint32_t>(sc.cuts.size() + sc.ll_cuts.size());
+    g.nkeyed = static_cast<uint32_t>(sc.cuts.size());
+    g.nitems = sc.nitems;
+    g.nll = sc.n_ll_send + sc.n_ll_recv;
+    g.R = static_cast<uint32_t>(R);
+    g.pad = 0;
+    std::memset(g.post, 0, sizeof g.post);
+    std::memset(g.send_post, 0, sizeof g.send_post);
+    for (int r = 0; r < R && r < static_cast<int>(sc.posts.size()); ++r) g.post[r] = sc.posts[static_cast<size_t>(r)];
+    for (int r = 0; r < R && r < static_cast<int>(sc.send_posts.size()); ++r)
+        g.send_post[r] = sc.send_posts[static_cast<size_t>(r)];
+    std::copy(sc.cuts.begin(), sc.cuts.end(), g.cuts);
+    std::copy(sc.ll_cuts.begin(), sc.ll_cuts.end(), g.cuts + sc.cuts.size());
+}
+
 CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& plan, const RankBuffers& rb,
                              cudaStream_t st) {
     std::vector<uint64_t> key = {plan_id, c->cfg.pipe_chunk, c->cfg.p2p_buffer,
@@ -716,14 +754,15 @@ CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& 
     cs.sc = build_schedule(plan, rb, c->cfg.pipe_chunk, slot_count(c->cfg), dchunk,
                            c->cfg.push_chunk ? c->cfg.push_chunk : kDefaultPushChunk, c->cfg.ll_max);
     // Recycle the least recently used entry that no CUDA graph holds, once
-    // kCachedSchedules of them exist: wait for its own last launch (its event,
-    // not a device-wide sync) and reuse its device buffers.
+    // kCachedSchedules of them exist: its buffers are rewritten on `st` after
+    // its last launch (a stream wait on its event -- no host block, no
+    // device-wide sync).
     size_t unpinned = 0;
     for (const CachedSchedule& e : c->schedules) unpinned += !e.pinned();
     if (unpinned >= kCachedSchedules) {
         for (auto it = std::prev(c->schedules.end());; --it) {
             if (!it->pinned()) {
-                it->wait_idle();
+                if (it->used) CUDA_TRY(cudaStreamWaitEvent(st, it->used, 0));
                 cs.items = std::move(it->items);
                 cs.posts = std::move(it->posts);
                 cs.send_posts = std::move(it->send_posts);
@@ -738,11 +777,27 @@ CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& 
         }
     }
     if (!cs.used) CUDA_TRY(cudaEventCreateWithFlags(&cs.used, cudaEventDisableTiming));
-    cs.items.assign(cs.sc.items, st);
-    cs.posts.assign(cs.sc.posts, st);
-    cs.send_posts.assign(cs.sc.send_posts, st);
     cs.finals.assign(cs.sc.final_waits, st);
-    cs.ll_items.assign(cs.sc.ll_items, st);
+    if (gen_on_device(cs.sc)) {
+        // the flows travel as kernel parameters; the device merges them
+        cs.items.reserve(cs.sc.nitems, st);
+        cs.ll_items.reserve(cs.sc.n_ll_send + cs.sc.n_ll_recv, st);
+        cs.posts.reserve(static_cast<size_t>(rb.R), st);
+        cs.send_posts.reserve(static_cast<size_t>(rb.R), st);
+        GenArgs g;
+        fill_gen(g, cs.sc, rb.R);
+        g.items = cs.items.p;
+        g.ll_items = cs.ll_items.p;
+        g.posts = cs.posts.p;
+        g.send_posts = cs.send_posts.p;
+        CUDA_TRY(launch_gen(g, st));
+    } else {
+        materialize(cs.sc);
+        cs.items.assign(cs.sc.items, st);
+        cs.posts.assign(cs.sc.posts, st);
+        cs.send_posts.assign(cs.sc.send_posts, st);
+        cs.ll_items.assign(cs.sc.ll_items, st);
+    }
     c->schedules.push_front(std::move(cs));
     return c->schedules.front();
 }
@@ -804,7 +859,7 @@ void pin_for_capture(CachedSchedule& cs, cudaStream_t st) {
 void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream_t st) {
     LaunchArgs a{};
     a.items = cs.items.p;
-    a.nitems = static_cast<uint32_t>(cs.sc.items.size());
+    a.nitems = cs.sc.nitems;
     a.slots = slot_count(c->cfg);
     a.pipe_chunk = c->cfg.pipe_chunk;
     a.epoch = 0;  // the kernel takes it from c->view.epoch (device), see engine.cu
@@ -838,7 +893,7 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     }
     int ctas = c->cfg.ctas > 0 ? c->cfg.ctas : c->sms_share;
     // small exchanges: no more CTAs than items (each CTA costs a fence at exit)
-    const size_t work = cs.sc.items.size() + cs.sc.ll_items.size();
+    const size_t work = static_cast<size_t>(cs.sc.nitems) + cs.sc.n_ll_send + cs.sc.n_ll_recv;
     ctas = std::max(1, std::min({ctas, c->sms, static_cast<int>(std::max<size_t>(work, 1))}));
     // every rank launches even with nothing to move: its posts and done
     // flags are what its peers wait for.  Launches of one comm share its
@@ -850,7 +905,7 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     CUDA_TRY(cudaStreamIsCapturing(st, &cap));
     const bool eager = cap == cudaStreamCaptureStatusNone;
     if (eager && c->launched && st != c->last_stream) CUDA_TRY(cudaStreamWaitEvent(st, c->last_launch, 0));
-    CUDA_TRY(launch_exchange(a, ctas, st));
+    CUDA_TRY(launch_exchange(a, ctas, st, c->colocated <= 1));
     if (eager) {
         CUDA_TRY(cudaEventRecord(c->last_launch, st));
         CUDA_TRY(cudaEventRecord(cs.used, st));

@@ -61,6 +61,24 @@ struct Item {
 };
 static_assert(sizeof(Item) == 32, "Item layout");
 
+// One flow of a rank's chunk schedule (schedule.cpp): item k covers bytes
+// [k * chunk, min((k + 1) * chunk, bytes)) of the flow and sorts by the key
+// (k + 0.5) / n + phase -- its progress fraction -- ties going to the larger
+// flow, then to the earlier insertion index base + k.  The host merges the
+// flows into the item list (schedule.cpp, ordered) or the device does
+// (engine.cu, gen_items_kernel) -- identical lists either way.
+enum CutFlags : uint32_t { kCutSrc = 1, kCutDst = 2, kCutPull = 4 };
+struct CutDesc {
+    Item proto;             // kind / peer / aux / pad of every item of the flow
+    uint64_t src0, dst0;    // item k: src = src0 + k * chunk (kCutSrc), dst = dst0 + k * chunk (kCutDst)
+    uint64_t bytes, chunk, n;
+    uint64_t src_from_dst;  // kCutPull: src = dst - src_from_dst (offset inside the sender's segment)
+    double phase;
+    uint32_t base;          // insertion index of item 0
+    uint32_t flags;         // CutFlags
+};
+static_assert(sizeof(CutDesc) == 96, "CutDesc layout");
+
 // Receive posts: where a sender's segment lands (+ a pull request bit).
 // Send posts: where my outgoing segment lives, if it is registered.
 enum PostMode : uint32_t {
@@ -174,6 +192,24 @@ struct CommDevice {
     DeviceStats* stats;           // null unless NIMBLE_STATS=1
     uint32_t* scratch;            // [0] queue head, [1] CTAs done, [2, 2+kMaxRanks) grant decisions
                                   // as sender, [2+kMaxRanks, 2+2*kMaxRanks) as receiver (kDecide*)
+};
+
+// Device-side schedule generation for a new matrix (engine.cu,
+// gen_items_kernel): the flows travel as kernel parameters, so a schedule
+// needs no host merge and no upload.  cuts[0, nkeyed) are merged into
+// items[0, nitems); cuts[nkeyed, ncuts) are the LL pieces (sends, then
+// receives), enumerated in order into ll_items.
+constexpr int kMaxGenCuts = 200;
+struct GenArgs {
+    Item* items;
+    Item* ll_items;
+    Post* posts;
+    Post* send_posts;
+    uint32_t ncuts, nkeyed, nitems, nll;
+    uint32_t R, pad;
+    Post post[kMaxRanks];
+    Post send_post[kMaxRanks];
+    CutDesc cuts[kMaxGenCuts];
 };
 
 // Per-launch arguments (passed by value as a __grid_constant__ kernel parameter).

@@ -916,6 +916,84 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
     }
 }
 
+// ---- device-side schedule generation (new matrices: no host merge, no upload) ----
+//
+// Item (f, k) of the keyed flows lands at position
+//     sum over flows g of #{k' : (g, k') before (f, k)}
+// in the merged list, with `before` the host merge's order (schedule.cpp):
+// key (k + 0.5) / n + phase, then the larger flow, then insertion index.  A
+// flow's keys increase with k, so each count is a prefix length, found from
+// a closed-form guess and a few exact comparisons.  Keys are computed with
+// the same IEEE operations as the host (correctly rounded divide and add,
+// no contraction), so the list is the host's, item for item.
+
+__device__ __forceinline__ double gen_key(const CutDesc& f, uint64_t k) {
+    return __dadd_rn(__ddiv_rn(static_cast<double>(k) + 0.5, static_cast<double>(f.n)), f.phase);
+}
+
+__device__ __forceinline__ bool gen_before(const CutDesc& a, uint64_t ka, double keya, const CutDesc& b, uint64_t kb,
+                                           double keyb) {
+    if (keya != keyb) return keya < keyb;
+    if (a.bytes != b.bytes) return a.bytes > b.bytes;
+    return a.base + ka < b.base + kb;
+}
+
+__device__ __forceinline__ Item gen_item(const CutDesc& f, uint64_t k) {
+    Item it = f.proto;
+    const uint64_t off = k * f.chunk;
+    it.src = (f.flags & kCutSrc) ? f.src0 + off : 0;
+    it.dst = (f.flags & kCutDst) ? f.dst0 + off : 0;
+    it.bytes = static_cast<uint32_t>(f.chunk < f.bytes - off ? f.chunk : f.bytes - off);
+    it.seq = static_cast<uint32_t>(k);
+    if (f.flags & kCutPull) it.src = it.dst - f.src_from_dst;
+    return it;
+}
+
+__global__ void __launch_bounds__(256) gen_items_kernel(const __grid_constant__ GenArgs g) {
+    __shared__ CutDesc cuts[kMaxGenCuts];
+    for (uint32_t i = threadIdx.x; i < g.ncuts; i += blockDim.x) cuts[i] = g.cuts[i];
+    if (blockIdx.x == 0)
+        for (uint32_t r = threadIdx.x; r < g.R; r += blockDim.x) {
+            g.posts[r] = g.post[r];
+            g.send_posts[r] = g.send_post[r];
+        }
+    __syncthreads();
+    const uint32_t total = g.nitems + g.nll;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < total; j += gridDim.x * blockDim.x) {
+        // the flow holding insertion index j (bases ascend within each group)
+        const bool ll = j >= g.nitems;
+        const uint32_t idx = ll ? j - g.nitems : j;
+        uint32_t lo = ll ? g.nkeyed : 0, hi = ll ? g.ncuts : g.nkeyed;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (cuts[mid].base <= idx) lo = mid;
+            else hi = mid;
+        }
+        const CutDesc& f = cuts[lo];
+        const uint64_t k = idx - f.base;
+        if (ll) {  // LL pieces keep their order: base is the slot in ll_items
+            g.ll_items[idx] = gen_item(f, k);
+            continue;
+        }
+        const double key = gen_key(f, k);
+        uint64_t pos = 0;
+        for (uint32_t h = 0; h < g.nkeyed; ++h) {
+            const CutDesc& c = cuts[h];
+            if (h == lo) {
+                pos += k;
+                continue;
+            }
+            // guess: k' with (k' + 0.5) / n + phase < key, then settle exactly
+            const double x = (key - c.phase) * static_cast<double>(c.n) - 0.5;
+            int64_t q = x <= 0.0 ? 0 : (x >= static_cast<double>(c.n) ? static_cast<int64_t>(c.n) : static_cast<int64_t>(ceil(x)));
+            while (q < static_cast<int64_t>(c.n) && gen_before(c, q, gen_key(c, q), f, k, key)) ++q;
+            while (q > 0 && !gen_before(c, q - 1, gen_key(c, q - 1), f, k, key)) --q;
+            pos += static_cast<uint64_t>(q);
+        }
+        g.items[pos] = gen_item(f, k);
+    }
+}
+
 // ---- payload fill / check (test and bench helpers) ----
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -966,7 +1044,7 @@ __global__ void check_kernel(const uint8_t* buf, uint64_t first, uint64_t n, uin
 
 // ---- host-side launchers (called from the comm runtime) ----
 
-cudaError_t launch_exchange(const LaunchArgs& args, int ctas, cudaStream_t stream) {
+cudaError_t launch_exchange(const LaunchArgs& args, int ctas, cudaStream_t stream, bool pdl) {
     static thread_local int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -985,8 +1063,18 @@ cudaError_t launch_exchange(const LaunchArgs& args, int ctas, cudaStream_t strea
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap with the previous exchange's tail
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, exchange_kernel, args);
+}
+
+cudaError_t launch_gen(const GenArgs& g, cudaStream_t st) {
+    const uint32_t total = g.nitems + g.nll;
+    if (!total && !g.R) return cudaSuccess;
+    uint32_t blocks = (total + 255) / 256;
+    if (blocks < 1) blocks = 1;
+    if (blocks > 1184) blocks = 1184;  // 8 x 148 SMs, grid-stride beyond
+    gen_items_kernel<<<blocks, 256, 0, st>>>(g);
+    return cudaGetLastError();
 }
 
 static int grid_for(uint64_t words) {

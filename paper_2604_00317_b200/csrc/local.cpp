@@ -4,6 +4,9 @@
 // path, with local addresses in place of peer ones.
 #include <cuda_runtime.h>
 
+#include <cstddef>
+#include <cstring>
+#include <list>
 #include <map>
 #include <mutex>
 #include <string>
@@ -15,17 +18,27 @@
 #include "schedule.hpp"
 
 namespace nb {
-cudaError_t launch_exchange(const LaunchArgs& args, int ctas, cudaStream_t stream);
+cudaError_t launch_exchange(const LaunchArgs& args, int ctas, cudaStream_t stream, bool pdl = true);
+cudaError_t launch_gen(const GenArgs& g, cudaStream_t st);
 
 namespace {
+
+// A generated item list for one (matrix, buffers, chunk): the last few are
+// kept, so alternating buffer sets (a pipelined caller) never rebuild.
+struct LocalEntry {
+    std::vector<uint64_t> key;
+    Item* items = nullptr;
+    size_t cap = 0, n = 0;
+    cudaEvent_t used = nullptr;  // after the entry's last launch
+};
+
+constexpr size_t kLocalEntries = 4;
 
 struct LocalCtx {
     bool ready = false;
     int sms = 148;
     CommDevice* d_view = nullptr;
-    std::vector<uint64_t> key;
-    Item* items = nullptr;
-    size_t cap = 0, n = 0;
+    std::list<LocalEntry> entries;  // most recently used first
 };
 
 std::mutex g_mu;
@@ -52,13 +65,62 @@ LocalCtx& context(int dev) {
     return c;
 }
 
+// The entry for `key`, generating its items on `st` when it is new: the
+// flows go to the device generator as kernel parameters (or, beyond its
+// capacity, are merged here and uploaded).  Reusing an old entry's buffer
+// waits for its last launch on the stream, not on the host.
+LocalEntry& entry_for(LocalCtx& c, const std::vector<uint64_t>& key, int R, const uint64_t* matrix,
+                      const std::vector<uint64_t>& sb, const std::vector<uint64_t>& rb, uint64_t chunk,
+                      cudaStream_t st) {
+    for (auto it = c.entries.begin(); it != c.entries.end(); ++it)
+        if (it->key == key) {
+            c.entries.splice(c.entries.begin(), c.entries, it);
+            return c.entries.front();
+        }
+    if (c.entries.size() >= kLocalEntries) {
+        c.entries.splice(c.entries.begin(), c.entries, std::prev(c.entries.end()));
+        check(cudaStreamWaitEvent(st, c.entries.front().used, 0), "cudaStreamWaitEvent");
+    } else {
+        c.entries.emplace_front();
+        check(cudaEventCreateWithFlags(&c.entries.front().used, cudaEventDisableTiming), "cudaEventCreate");
+    }
+    LocalEntry& e = c.entries.front();
+    e.key = key;
+    std::vector<CutDesc> cuts = build_local_cuts(R, matrix, sb.data(), rb.data(), chunk);
+    size_t n = 0;
+    for (const CutDesc& f : cuts) n += f.n;
+    if (n > e.cap) {
+        if (e.items) check(cudaFreeAsync(e.items, st), "cudaFreeAsync");
+        e.items = nullptr;
+        check(cudaMallocAsync(reinterpret_cast<void**>(&e.items), n * sizeof(Item), st), "cudaMallocAsync");
+        e.cap = n;
+    }
+    e.n = n;
+    if (!n) return e;
+    if (cuts.size() <= static_cast<size_t>(kMaxGenCuts)) {
+        GenArgs g;
+        std::memset(&g, 0, offsetof(GenArgs, cuts));
+        g.items = e.items;
+        g.ncuts = g.nkeyed = static_cast<uint32_t>(cuts.size());
+        g.nitems = static_cast<uint32_t>(n);
+        std::copy(cuts.begin(), cuts.end(), g.cuts);
+        check(launch_gen(g, st), "schedule generation");
+    } else {
+        std::vector<Item> items = merge_cuts(cuts);
+        check(cudaMemcpyAsync(e.items, items.data(), n * sizeof(Item), cudaMemcpyHostToDevice, st), "cudaMemcpy");
+        check(cudaStreamSynchronize(st), "cudaStreamSynchronize");  // `items` is pageable and dies here
+    }
+    return e;
+}
+
 }  // namespace
 }  // namespace nb
 
 extern "C" nimbleResult_t nimbleExchangeLocal(int R, const void* const* sendbuffs, void* const* recvbuffs,
                                               const uint64_t* matrix, int ctas, void* stream) {
     return nb::guarded([&] {
-        if (R < 1 || !sendbuffs || !recvbuffs || !matrix) throw nb::Error(nimbleInvalidArgument, "local: bad argument");
+        if (R < 1 || R > nb::kMaxRanks || !sendbuffs || !recvbuffs || !matrix)
+            throw nb::Error(nimbleInvalidArgument, "local: bad argument");
         int dev = 0;
         nb::check(cudaGetDevice(&dev), "cudaGetDevice");
         std::lock_guard<std::mutex> lock(nb::g_mu);
@@ -75,23 +137,10 @@ extern "C" nimbleResult_t nimbleExchangeLocal(int R, const void* const* sendbuff
         key.insert(key.end(), sb.begin(), sb.end());
         key.insert(key.end(), rb.begin(), rb.end());
         key.push_back(chunk);
-        if (key != c.key) {
-            std::vector<nb::Item> items = nb::build_local_items(R, matrix, sb.data(), rb.data(), chunk);
-            nb::check(cudaStreamSynchronize(st), "cudaStreamSynchronize");  // previous launch may read the list
-            if (items.size() > c.cap) {
-                if (c.items) cudaFree(c.items);
-                nb::check(cudaMalloc(&c.items, items.size() * sizeof(nb::Item)), "cudaMalloc");
-                c.cap = items.size();
-            }
-            if (!items.empty())
-                nb::check(cudaMemcpy(c.items, items.data(), items.size() * sizeof(nb::Item), cudaMemcpyHostToDevice),
-                          "cudaMemcpy");
-            c.n = items.size();
-            c.key = key;
-        }
+        nb::LocalEntry& e = nb::entry_for(c, key, R, matrix, sb, rb, chunk, st);
         nb::LaunchArgs a{};
-        a.items = c.items;
-        a.nitems = static_cast<uint32_t>(c.n);
+        a.items = e.items;
+        a.nitems = static_cast<uint32_t>(e.n);
         a.slots = 1;
         a.pipe_chunk = chunk;
         a.comm = c.d_view;
@@ -99,5 +148,6 @@ extern "C" nimbleResult_t nimbleExchangeLocal(int R, const void* const* sendbuff
         int g = ctas > 0 ? ctas : c.sms;
         if (g > c.sms) g = c.sms;
         nb::check(nb::launch_exchange(a, g, st), "exchange launch");
+        nb::check(cudaEventRecord(e.used, st), "cudaEventRecord");
     });
 }

@@ -10,52 +10,38 @@ namespace nb {
 
 namespace {
 
-// One flow's items, generated when they are merged: item k covers bytes
-// [k * chunk, min((k + 1) * chunk, bytes)) and sorts by the key
-// (k + 0.5) / n + phase -- its progress fraction.
-struct FlowCut {
-    Item proto;
-    uint64_t src0, dst0, bytes, chunk, n;
-    double phase;
-    uint32_t base;          // insertion order of item 0: the deterministic tie break
-    bool pull;              // pulls: src = dst - src_from_dst (offset inside the sender's segment)
-    uint64_t src_from_dst;
-};
-
 struct Cuts {
-    std::vector<FlowCut> flows;
+    std::vector<CutDesc> flows;
     uint32_t count = 0;  // items so far
 };
 
-// Appends one flow; returns its item count.
+// Appends one flow (device.cuh CutDesc); returns its item count.
 uint32_t cut(Cuts& out, Item proto, uint64_t src0, uint64_t dst0, uint64_t bytes, uint64_t chunk, double phase,
              bool pull = false, uint64_t src_from_dst = 0) {
     const uint64_t n = (bytes + chunk - 1) / chunk;
-    if (n) out.flows.push_back({proto, src0, dst0, bytes, chunk, n, phase, out.count, pull, src_from_dst});
+    if (n) {
+        CutDesc c{};
+        c.proto = proto;
+        c.src0 = src0;
+        c.dst0 = dst0;
+        c.bytes = bytes;
+        c.chunk = chunk;
+        c.n = n;
+        c.src_from_dst = src_from_dst;
+        c.phase = phase;
+        c.base = out.count;
+        c.flags = (src0 ? static_cast<uint32_t>(kCutSrc) : 0u) | kCutDst | (pull ? static_cast<uint32_t>(kCutPull) : 0u);
+        out.flows.push_back(c);
+    }
     out.count += static_cast<uint32_t>(n);
     return static_cast<uint32_t>(n);
 }
 
-Item item_of(const FlowCut& f, uint64_t k) {
-    Item it = f.proto;
-    const uint64_t off = k * f.chunk;
-    it.src = f.src0 ? f.src0 + off : 0;
-    it.dst = f.dst0 + off;
-    it.bytes = static_cast<uint32_t>(std::min(f.chunk, f.bytes - off));
-    it.seq = static_cast<uint32_t>(k);
-    if (f.pull) it.src = it.dst - f.src_from_dst;
-    return it;
-}
-
 struct Cursor {
     double key;
-    const FlowCut* f;
+    const CutDesc* f;
     uint64_t k;
 };
-
-double key_of(const FlowCut& f, uint64_t k) {
-    return (static_cast<double>(k) + 0.5) / static_cast<double>(f.n) + f.phase;
-}
 
 // Strict, total order: key, then hot (larger) flows first on ties, then insertion order.
 bool before(const Cursor& a, const Cursor& b) {
@@ -64,31 +50,60 @@ bool before(const Cursor& a, const Cursor& b) {
     return a.f->base + a.k < b.f->base + b.k;
 }
 
+}  // namespace
+
+Item cut_item(const CutDesc& f, uint64_t k) {
+    Item it = f.proto;
+    const uint64_t off = k * f.chunk;
+    it.src = (f.flags & kCutSrc) ? f.src0 + off : 0;
+    it.dst = (f.flags & kCutDst) ? f.dst0 + off : 0;
+    it.bytes = static_cast<uint32_t>(std::min(f.chunk, f.bytes - off));
+    it.seq = static_cast<uint32_t>(k);
+    if (f.flags & kCutPull) it.src = it.dst - f.src_from_dst;
+    return it;
+}
+
+double cut_key(const CutDesc& f, uint64_t k) {
+    return (static_cast<double>(k) + 0.5) / static_cast<double>(f.n) + f.phase;
+}
+
 // All items in `before` order: a k-way merge over the flows (each one's keys
 // increase with k), generating items as they are emitted -- O(n log flows)
-// with no per-item sort records, which matters when every call brings a new
-// matrix (35-53k items at 256 MiB per rank).
-std::vector<Item> ordered(const Cuts& cuts) {
+// with no per-item sort records.
+std::vector<Item> merge_cuts(const std::vector<CutDesc>& flows) {
     std::vector<Cursor> heap;
-    heap.reserve(cuts.flows.size());
-    for (const FlowCut& f : cuts.flows) heap.push_back({key_of(f, 0), &f, 0});
+    heap.reserve(flows.size());
+    uint64_t total = 0;
+    for (const CutDesc& f : flows) {
+        heap.push_back({cut_key(f, 0), &f, 0});
+        total += f.n;
+    }
     auto later = [](const Cursor& a, const Cursor& b) { return before(b, a); };  // min-heap
     std::make_heap(heap.begin(), heap.end(), later);
     std::vector<Item> items;
-    items.reserve(cuts.count);
+    items.reserve(total);
     while (!heap.empty()) {
         std::pop_heap(heap.begin(), heap.end(), later);
         Cursor& c = heap.back();
-        items.push_back(item_of(*c.f, c.k));
+        items.push_back(cut_item(*c.f, c.k));
         if (++c.k == c.f->n) {
             heap.pop_back();
         } else {
-            c.key = key_of(*c.f, c.k);
+            c.key = cut_key(*c.f, c.k);
             std::push_heap(heap.begin(), heap.end(), later);
         }
     }
     return items;
 }
+
+void materialize(Schedule& sc) {
+    sc.items = merge_cuts(sc.cuts);
+    sc.ll_items.clear();
+    for (const CutDesc& f : sc.ll_cuts)
+        for (uint64_t k = 0; k < f.n; ++k) sc.ll_items.push_back(cut_item(f, k));
+}
+
+namespace {
 
 constexpr double kHop2 = 1e-9;  // forward of chunk k sorts right after its stage-in
 
@@ -129,7 +144,7 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
         sc.moved_bytes += rb.send_bytes[me];
     }
 
-    std::vector<Item> ll_recv;
+    Cuts ll_send, ll_recv;
     for (const PairRoutes& pr : plan.pairs) {
         const int s = pr.src, d = pr.dst;
         if ((s == me || d == me) && ll_pair(plan, s, d, pr.demand, ll_max)) {
@@ -137,25 +152,21 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
                 throw Error(nimbleInvalidArgument, "schedule: plan demand differs from the send count");
             if (d == me && pr.demand != rb.recv_bytes[s])
                 throw Error(nimbleInvalidArgument, "alltoallv: receive count differs from the planned demand");
-            for (uint64_t off = 0; off < pr.demand; off += kLLPiece) {  // pieces: several CTAs per pair
-                Item it{};
-                it.bytes = static_cast<uint32_t>(std::min<uint64_t>(kLLPiece, pr.demand - off));
-                it.seq = static_cast<uint32_t>(off / kLLPiece);
-                it.pad = static_cast<uint32_t>(pr.demand);
-                if (s == me) {
-                    it.kind = kLLSend;
-                    it.peer = static_cast<uint8_t>(d);
-                    it.src = rb.send_ptr[d] + off;
-                    sc.ll_items.push_back(it);
-                } else {
-                    it.kind = kLLRecv;
-                    it.peer = static_cast<uint8_t>(s);
-                    it.dst = rb.recv_ptr[s] + off;
-                    ll_recv.push_back(it);
-                }
+            // pieces of kLLPiece bytes: several CTAs per pair; the pair size rides in pad
+            Item proto{};
+            proto.pad = static_cast<uint32_t>(pr.demand);
+            if (s == me) {
+                proto.kind = kLLSend;
+                proto.peer = static_cast<uint8_t>(d);
+                cut(ll_send, proto, rb.send_ptr[d], 0, pr.demand, kLLPiece, 0.0);
+                ll_send.flows.back().flags = kCutSrc;  // no destination address: the receiver's LL slot
+                sc.moved_bytes += pr.demand;
+            } else {
+                proto.kind = kLLRecv;
+                proto.peer = static_cast<uint8_t>(s);
+                cut(ll_recv, proto, 0, rb.recv_ptr[s], pr.demand, kLLPiece, 0.0);
+                sc.ll_senders |= 1ull << s;
             }
-            if (s == me) sc.moved_bytes += pr.demand;
-            else sc.ll_senders |= 1ull << s;
             continue;
         }
         if (s != me && d != me) {
@@ -238,15 +249,18 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
             off += bytes;
         }
     }
-    sc.items = ordered(keyed);
-    sc.n_ll_send = static_cast<uint32_t>(sc.ll_items.size());
-    sc.n_ll_recv = static_cast<uint32_t>(ll_recv.size());
-    sc.ll_items.insert(sc.ll_items.end(), ll_recv.begin(), ll_recv.end());
+    sc.cuts = std::move(keyed.flows);
+    sc.nitems = keyed.count;
+    sc.n_ll_send = ll_send.count;
+    sc.n_ll_recv = ll_recv.count;
+    sc.ll_cuts = std::move(ll_send.flows);
+    for (CutDesc& f : ll_recv.flows) f.base += ll_send.count;  // base = the piece's slot in ll_items
+    sc.ll_cuts.insert(sc.ll_cuts.end(), ll_recv.flows.begin(), ll_recv.flows.end());
     return sc;
 }
 
-std::vector<Item> build_local_items(int R, const uint64_t* m, const uint64_t* send_base, const uint64_t* recv_base,
-                                    uint64_t chunk) {
+std::vector<CutDesc> build_local_cuts(int R, const uint64_t* m, const uint64_t* send_base, const uint64_t* recv_base,
+                                      uint64_t chunk) {
     Cuts keyed;
     for (int s = 0; s < R; ++s) {
         uint64_t soff = 0;
@@ -263,7 +277,7 @@ std::vector<Item> build_local_items(int R, const uint64_t* m, const uint64_t* se
             soff += b;
         }
     }
-    return ordered(keyed);
+    return std::move(keyed.flows);
 }
 
 }  // namespace nb

@@ -32,8 +32,11 @@ struct RankBuffers {
 };
 
 struct Schedule {
-    std::vector<Item> items;
-    std::vector<Item> ll_items;  // LL sends, then LL receives (engine: LaunchArgs::ll_items)
+    std::vector<CutDesc> cuts;     // the keyed flows (merged into the item list)
+    std::vector<CutDesc> ll_cuts;  // LL sends, then LL receives (pieces enumerated in order)
+    uint32_t nitems = 0;           // items of the keyed flows
+    std::vector<Item> items;       // materialize(): the merged list (host)
+    std::vector<Item> ll_items;    // materialize(): LL sends, then LL receives (engine: LaunchArgs::ll_items)
     uint32_t n_ll_send = 0, n_ll_recv = 0;
     uint64_t ll_senders = 0;
     std::vector<Post> posts;
@@ -54,13 +57,22 @@ struct Schedule {
 Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t pipe_chunk, uint32_t slots,
                         uint64_t direct_chunk, uint64_t push_chunk = 0, uint64_t ll_max = 0);
 
+// Item k of a flow, its key, and the host merge of the flows into the item
+// list (`before` order) -- what the device generator reproduces.
+Item cut_item(const CutDesc& f, uint64_t k);
+double cut_key(const CutDesc& f, uint64_t k);
+std::vector<Item> merge_cuts(const std::vector<CutDesc>& flows);
+// Fill sc.items / sc.ll_items on the host from the cuts.
+void materialize(Schedule& sc);
+
 // Does pair (s, d) of `bytes` ride the LL protocol?  Both endpoints decide
 // alike from what they both know: the pair size and the replicated plan
 // (0 < bytes <= ll_max, no relay route).
 bool ll_pair(const PlanResult& plan, int s, int d, uint64_t bytes, uint64_t ll_max);
 
-// 1-GPU emulated exchange: every pair's segment as local copies (packed layout).
-std::vector<Item> build_local_items(int R, const uint64_t* matrix, const uint64_t* send_base,
-                                    const uint64_t* recv_base, uint64_t chunk);
+// 1-GPU emulated exchange: every pair's segment as local copies (packed
+// layout), as flows (merge_cuts gives the item list).
+std::vector<CutDesc> build_local_cuts(int R, const uint64_t* matrix, const uint64_t* send_base,
+                                      const uint64_t* recv_base, uint64_t chunk);
 
 }  // namespace nb

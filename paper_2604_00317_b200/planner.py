@@ -321,10 +321,13 @@ def port_bound_seconds(matrix, ranks, port_bytes_per_s=900e9):
 
 
 def debug_schedule(topo: Topology, ranks, ranks_per_node, matrix, rank, config: PlannerConfig | None = None,
-                   pipe_chunk=64 * KiB, slots=160, direct_chunk=64 * KiB, staged_mask=0, pull_mask=0, push_chunk=0):
+                   pipe_chunk=64 * KiB, slots=160, direct_chunk=64 * KiB, staged_mask=0, pull_mask=0, push_chunk=0,
+                   device=False):
     """The chunk scheduler's ordered work items for `rank` (nimbleDebugSchedule).
 
-    push_chunk = 0 cuts direct pushes at direct_chunk.  Returns a list of
+    push_chunk = 0 cuts direct pushes at direct_chunk.  device=True merges the
+    flows with the GPU generator instead (nimbleDebugScheduleDevice; needs a
+    GPU) -- the list must be the same.  Returns a list of
     dicts (kind, peer, aux, seq, src, dst, bytes).  The plan
     is mcf_plan on `topo` over the off-diagonal demands (self segments are
     plain local copies and are not part of it).
@@ -336,12 +339,11 @@ def debug_schedule(topo: Topology, ranks, ranks_per_node, matrix, rank, config: 
               ctypes.byref(h))
     try:
         n = c_int()
-        _lib.call("nimbleDebugSchedule", h, rank, ranks, pipe_chunk, slots, direct_chunk, push_chunk, staged_mask,
-                  pull_mask,
+        fn = "nimbleDebugScheduleDevice" if device else "nimbleDebugSchedule"
+        _lib.call(fn, h, rank, ranks, pipe_chunk, slots, direct_chunk, push_chunk, staged_mask, pull_mask,
                   None, 0, ctypes.byref(n))
         items = (_lib.Item * max(n.value, 1))()
-        _lib.call("nimbleDebugSchedule", h, rank, ranks, pipe_chunk, slots, direct_chunk, push_chunk, staged_mask,
-                  pull_mask,
+        _lib.call(fn, h, rank, ranks, pipe_chunk, slots, direct_chunk, push_chunk, staged_mask, pull_mask,
                   items, n.value, ctypes.byref(n))
     finally:
         _lib.lib().nimblePlanDestroy(h)

@@ -125,7 +125,9 @@ def _entry(fn, rank, world, port, q, args):
 
 def _thread_server(R, conn):
     """Long-lived child process: runs worker calls as R threads on GPU 0."""
-    os.environ.update(NIMBLE_TIMEOUT_MS="15000", NIMBLE_STATS="1")
+    # one hardware queue per stream: R ranks' streams must not alias onto one
+    # queue (a spinning grid would block the peer grid queued behind it)
+    os.environ.update(NIMBLE_TIMEOUT_MS="15000", NIMBLE_STATS="1", CUDA_DEVICE_MAX_CONNECTIONS="32")
     torch.cuda.set_device(0)
     from paper_2604_00317_b200 import comm as C
     while True:
@@ -269,9 +271,10 @@ def _slots(comm):
 
 def _rings_bounded(comm):
     """Device-side bounded-buffer check of every staging ring this rank fed
-    since the last call (reference tests/acceptance.cpp:270-288: occupancy
-    <= S; and no slot claimed while its previous chunk was undrained)."""
-    st = comm.stats(reset=True)
+    since the comm's counters were last reset (reference
+    tests/acceptance.cpp:270-288: occupancy <= S; and no slot claimed while
+    its previous chunk was undrained)."""
+    st = comm.stats()
     return st["slot_double_claims"] == 0 and st["slot_max_occupancy"] <= _slots(comm)
 
 
@@ -751,7 +754,7 @@ def w_relay_split(comm, rank, R, nbytes):
     comm.stats(reset=True)
     m = P.gen_p2p(R, 0, 1, nbytes)
     bad, ok = _exchange_and_check(comm, rank, R, m, True, 23, host_check=nbytes <= 256 * MiB)
-    st = comm.stats(reset=True)  # _exchange_and_check already read / reset the ring counters
+    st = comm.stats(reset=True)
     comm.set_config(fabric="nvswitch")
     return bad, ok, {k: st[k] for k in ("push", "stage", "forward", "pull", "drain")}
 

@@ -10,6 +10,8 @@ import hashlib
 import json
 import os
 
+import pytest
+
 from paper_2604_00317_b200 import planner as P
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -17,7 +19,7 @@ GOLDEN = os.path.join(HERE, "golden", "schedule_hashes.json")
 MiB = 1 << 20
 
 
-def _hashes():
+def _hashes(device=False):
     out = {}
     cases = []
     for R in (2, 3, 4, 8):
@@ -29,7 +31,8 @@ def _hashes():
             topo = P.build_canonical(1, R, 0, 900e9, 0, fab)
             for rank in range(R):
                 for staged, pull, pc in ((0, 0, 0), (0b0110, 0b1001, 8192), ((1 << R) - 1, 0, 8192)):
-                    items = P.debug_schedule(topo, R, R, m, rank, staged_mask=staged, pull_mask=pull, push_chunk=pc)
+                    items = P.debug_schedule(topo, R, R, m, rank, staged_mask=staged, pull_mask=pull, push_chunk=pc,
+                                             device=device)
                     key = f"{name}-{R}-{r:.3f}-{fab}-{rank}-{staged}-{pull}-{pc}"
                     out[key] = hashlib.sha1(json.dumps(items).encode()).hexdigest()
     return out
@@ -45,3 +48,17 @@ def test_schedules_match_pinned_hashes(lib):
     assert set(got) == set(want)
     diff = [k for k in want if got[k] != want[k]]
     assert not diff, f"{len(diff)} schedules changed, e.g. {diff[:3]}"
+
+
+@pytest.mark.gpu
+def test_device_generator_reproduces_pinned_schedules(lib):
+    """The GPU merge (engine.cu gen_items_kernel), which schedules every new
+    matrix of a communicator, emits the same 510 item lists as the host merge."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    with open(GOLDEN) as f:
+        want = json.load(f)
+    got = _hashes(device=True)
+    diff = [k for k in want if got[k] != want[k]]
+    assert not diff, f"{len(diff)} schedules differ from the host merge, e.g. {diff[:3]}"
