@@ -314,8 +314,14 @@ def run_local(args):
     per_step = [ev[k].elapsed_time(ev[k + 1]) * 1e-3 for k in range(args.steps)]
     t_total = ev[0].elapsed_time(ev[-1]) * 1e-3
     moved = sum(sum(step_m(k)) for k in range(args.steps))
-    # verify the last step's delivery
+    # verify the last step's matrix: payload laid out for it, one more exchange
     last = step_m(args.steps - 1)
+    if mats:
+        for s in range(R):
+            sc, sd, _, _ = C.packed_displs(last, R, s)
+            for d in range(R):
+                C.fill_payload(sends[s][sd[d]:], 0, sc[d], 1, s, d)
+        C.exchange_local(sends, recvs, last, args.ctas, stream)
     bad = torch.zeros(1, dtype=torch.int64, device="cuda")
     for d in range(R):
         _, _, rc, rd = C.packed_displs(last, R, d)
@@ -457,7 +463,11 @@ def run_multi(args):
     host_us = max_over_ranks(statistics.median(host_s) * 1e6)
     moved = sum(sum(mats[k]) for k in range(args.steps)) if mats else total * args.steps
     comm.check_async()
-    _, _, lrc, lrd = lay(args.steps - 1)
+    lsc, lsd, lrc, lrd = lay(args.steps - 1)
+    if mats:  # payload laid out for the last matrix, one more exchange
+        for d in range(R):
+            C.fill_payload(send[lsd[d]:], 0, lsc[d], 1, rank, d)
+        comm.alltoallv(send, lsc, lsd, recv, lrc, lrd, stream)
     bad = torch.zeros(1, dtype=torch.int64, device="cuda")
     for s in range(R):
         C.check_payload(recv[lrd[s]:], 0, lrc[s], 1, s, rank, bad)

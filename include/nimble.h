@@ -353,6 +353,11 @@ typedef struct {
     uint64_t slot_double_claims;
     uint64_t slot_claims;
     uint64_t pad;
+    /* host side: the C ABI's cost per data-path call (nimbleAlltoAllv /
+     * grouped send-recv), and the plans / schedules built for new matrices */
+    uint64_t host_calls, host_ns, host_ns_max;
+    uint64_t plans_built, plan_ns, schedules_built, schedule_ns;
+    uint64_t host_pad;
 } nimbleCommStats;
 nimbleResult_t nimbleCommGetStats(nimbleComm_t comm, nimbleCommStats* stats, int reset);
 

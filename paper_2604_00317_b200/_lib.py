@@ -60,7 +60,9 @@ class BenchResult(ctypes.Structure):  # nimbleBenchResult
 
 class CommStats(ctypes.Structure):  # nimbleCommStats
     _fields_ = [("bytes", (c_u64 * 32) * 8), ("items", (c_u64 * 32) * 8), ("slot_max_occupancy", c_u64),
-                ("slot_double_claims", c_u64), ("slot_claims", c_u64), ("pad", c_u64)]
+                ("slot_double_claims", c_u64), ("slot_claims", c_u64), ("pad", c_u64),
+                ("host_calls", c_u64), ("host_ns", c_u64), ("host_ns_max", c_u64), ("plans_built", c_u64),
+                ("plan_ns", c_u64), ("schedules_built", c_u64), ("schedule_ns", c_u64), ("host_pad", c_u64)]
 
 
 # name -> argtypes (restype is always nimbleResult_t unless listed in _RESTYPES)

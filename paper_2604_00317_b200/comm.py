@@ -147,7 +147,9 @@ class Comm:
         st = _lib.CommStats()
         _lib.call("nimbleCommGetStats", self._h, ctypes.byref(st), 1 if reset else 0)
         out = {"slot_max_occupancy": st.slot_max_occupancy, "slot_double_claims": st.slot_double_claims,
-               "slot_claims": st.slot_claims}
+               "slot_claims": st.slot_claims, "host_calls": st.host_calls, "host_ns": st.host_ns,
+               "host_ns_max": st.host_ns_max, "plans_built": st.plans_built, "plan_ns": st.plan_ns,
+               "schedules_built": st.schedules_built, "schedule_ns": st.schedule_ns}
         for k, name in enumerate(self.STAT_KINDS):
             out[name] = [int(st.bytes[k][p]) for p in range(self.nranks)]
             out[name + "_items"] = [int(st.items[k][p]) for p in range(self.nranks)]

@@ -296,6 +296,9 @@ struct nimbleComm {
     cudaStream_t bench_stream = nullptr;
     uint64_t* d_trace = nullptr;  // NIMBLE_TRACE=1: device timeline of the last launch
     nb::DeviceStats* d_stats = nullptr;  // NIMBLE_STATS=1: per-kind byte counters, slot occupancy
+    struct {
+        uint64_t calls = 0, ns = 0, ns_max = 0, plans = 0, plan_ns = 0, schedules = 0, schedule_ns = 0;
+    } host;  // C ABI cost per data-path call (nimbleCommGetStats)
     cudaEvent_t last_launch = nullptr;  // launches on one comm are serialized across streams
     cudaStream_t last_stream = nullptr;
     bool launched = false;
@@ -330,6 +333,8 @@ struct Clique {
     }
 };
 
+uint64_t ring_count(const nimbleComm* c, const nimbleCommConfig& cfg);
+
 void upload_view(nimbleComm* c) {
     c->view.rank = c->rank;
     c->view.nranks = c->nranks;
@@ -342,6 +347,7 @@ void upload_view(nimbleComm* c) {
     c->view.status = c->d_status;
     c->view.scratch = c->d_scratch;
     c->view.stats = c->d_stats;
+    c->view.ring_full = ring_count(c, c->cfg) > static_cast<uint64_t>(c->nranks) ? 1u : 0u;
     c->view.epoch = c->d_epoch;
     const char* t = std::getenv("NIMBLE_TIMEOUT_MS");
     c->view.timeout_ms = t && *t ? static_cast<uint32_t>(std::atoi(t)) : 60000u;
@@ -364,8 +370,27 @@ uint32_t slot_count(const nimbleCommConfig& cfg) {
     return static_cast<uint32_t>(s);
 }
 
+// Staging rings hosted per rank.  Under the nvswitch model the planner never
+// relays, so a rank hosts only its self rings -- one per sender, fed by
+// pushes into an unregistered receive buffer: R rings (80 MiB at R = 8 with
+// the 10 MiB reference geometry).  The mesh model may route any pair through
+// any rank: R x R rings (ring (s, d) at index s * R + d).
+uint64_t ring_count(const nimbleComm* c, const nimbleCommConfig& cfg) {
+    const uint64_t R = static_cast<uint64_t>(c->nranks);
+    return cfg.fabric == nimbleFabricAllToAll ? R * R : R;
+}
+
 uint64_t staging_size(const nimbleComm* c) {
-    return static_cast<uint64_t>(c->nranks) * c->nranks * slot_count(c->cfg) * c->cfg.pipe_chunk;
+    return ring_count(c, c->cfg) * slot_count(c->cfg) * c->cfg.pipe_chunk;
+}
+
+// Hash of the data-path geometry every rank must share: where chunks land in
+// rings and slots, how pairs are cut, which pairs ride LL, which model plans.
+uint64_t geometry_hash(const nimbleCommConfig& cfg) {
+    const uint64_t v[] = {cfg.pipe_chunk, cfg.p2p_buffer, static_cast<uint64_t>(cfg.channels_per_peer),
+                          cfg.push_chunk, cfg.direct_chunk, cfg.ll_max, static_cast<uint64_t>(cfg.fabric),
+                          static_cast<uint64_t>(cfg.gpus_per_node)};
+    return fnv(v, sizeof v);
 }
 
 void default_config(nimbleCommConfig* cfg, int nranks) {
@@ -528,10 +553,20 @@ std::shared_ptr<PlanResult> plan_for(nimbleComm* c, const std::vector<uint64_t>&
             *plan_id = it->id;
             return it->plan;
         }
+    const auto t0 = std::chrono::steady_clock::now();
     const LinkModel lm = comm_model(c);
     Demand d;
     d.ranks = c->nranks;
     d.bytes = matrix;
+    struct Timed {
+        nimbleComm* c;
+        std::chrono::steady_clock::time_point t0;
+        ~Timed() {
+            ++c->host.plans;
+            c->host.plan_ns += static_cast<uint64_t>(
+                std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count());
+        }
+    } timed{c, t0};
     // On the nvswitch model every pair has exactly one candidate (direct), so
     // the MCF sweep can only put each pair's demand on it: the direct plan has
     // the same flows (tests/test_planner_parity.py) at a fraction of the cost
@@ -747,6 +782,16 @@ CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& 
         throw Error(nimbleInvalidUsage, "graph capture: run the same exchange once before capturing it "
                                         "(its schedule must be cached; capture does not allow uploads)");
     c->fast.cs = nullptr;  // entries may be recycled below
+    const auto t0 = std::chrono::steady_clock::now();
+    struct Timed {
+        nimbleComm* c;
+        std::chrono::steady_clock::time_point t0;
+        ~Timed() {
+            ++c->host.schedules;
+            c->host.schedule_ns += static_cast<uint64_t>(
+                std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count());
+        }
+    } timed{c, t0};
     reap_retired(c);
     CachedSchedule cs;
     cs.key = key;
@@ -917,6 +962,15 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
 }
 
 void run_exchanges(std::vector<Exchange>& exs) {
+    // single-process cliques: the members in this group must share the
+    // data-path geometry (multi-process comms check it in SetConfig)
+    for (Exchange& ex : exs)
+        if (ex.comm->clique)
+            for (Exchange& other : exs)
+                if (other.comm->clique == ex.comm->clique &&
+                    geometry_hash(other.comm->cfg) != geometry_hash(ex.comm->cfg))
+                    throw Error(nimbleInvalidUsage, "group: comms of one clique disagree on the data-path geometry "
+                                                    "(set the same config on every member)");
     // full demand matrix when the planner's model can route through relays
     std::map<nimbleComm*, std::vector<uint64_t>> full;
     for (Exchange& ex : exs) {
@@ -1358,11 +1412,36 @@ nimbleResult_t nimbleCommSetConfig(nimbleComm_t c, const nimbleCommConfig* cfg) 
         if (next.ll_max > nb::kLLMaxData)
             throw nb::Error(nimbleInvalidArgument, "config: ll_max above the LL slot size (1 MiB)");
         const bool regrow = next.pipe_chunk != c->cfg.pipe_chunk || next.p2p_buffer != c->cfg.p2p_buffer ||
-                            next.channels_per_peer != c->cfg.channels_per_peer;
+                            next.channels_per_peer != c->cfg.channels_per_peer ||
+                            nb::ring_count(c, next) != nb::ring_count(c, c->cfg);
         nb::DeviceGuard g(c->device);
-        if (regrow && c->clique)
-            throw nb::Error(nimbleInvalidUsage, "config: staging geometry is fixed for single-process comms");
-        if (regrow) {
+        if (c->boot) {  // collective: every rank must bring the same data-path geometry
+            const uint64_t mine = nb::geometry_hash(next);
+            std::vector<uint64_t> all(static_cast<size_t>(c->nranks));
+            c->boot->allgather(&mine, sizeof mine, all.data());
+            for (uint64_t h : all)
+                if (h != mine)
+                    throw nb::Error(nimbleInvalidUsage, "config: ranks disagree on the data-path geometry "
+                                                        "(chunk sizes, staging, LL limit, fabric model)");
+        }
+        if (regrow && c->clique) {
+            // one process: swap my staging region under every member's view
+            // (they are idle between grouped calls; wait for their last launches)
+            for (nimbleComm* p : c->clique->comms) {
+                nb::DeviceGuard pg(p->device);
+                nb::quiesce(p);
+            }
+            c->cfg = next;
+            CUDA_TRY(cudaFree(c->staging));
+            c->staging = nullptr;
+            c->staging_bytes = nb::staging_size(c);
+            CUDA_TRY(cudaMalloc(&c->staging, std::max<uint64_t>(c->staging_bytes, 256)));
+            for (nimbleComm* p : c->clique->comms) {
+                p->peer_staging[static_cast<size_t>(c->rank)] = c->staging;
+                nb::DeviceGuard pg(p->device);
+                nb::upload_view(p);
+            }
+        } else if (regrow) {
             nb::quiesce(c);
             if (c->boot) c->boot->barrier();
             nb::free_regions(c);  // nulls the pointers: a failing setup below leaves nothing to double-free
@@ -1372,6 +1451,7 @@ nimbleResult_t nimbleCommSetConfig(nimbleComm_t c, const nimbleCommConfig* cfg) 
             nb::upload_view(c);
         }
         c->cfg = next;
+        nb::upload_view(c);
         c->plans.clear();
         nb::drop_schedules(c);
         if (c->boot) c->boot->barrier();
@@ -1453,6 +1533,19 @@ nimbleResult_t nimbleRecv(void* recvbuff, size_t count, nimbleDataType_t dt, int
 nimbleResult_t nimbleAlltoAllv(const void* sendbuff, const size_t sendcounts[], const size_t sdispls[], void* recvbuff,
                                const size_t recvcounts[], const size_t rdispls[], nimbleDataType_t dt,
                                nimbleComm_t comm, void* stream) {
+    const auto t0 = std::chrono::steady_clock::now();
+    struct Timed {
+        nimbleComm* c;
+        std::chrono::steady_clock::time_point t0;
+        ~Timed() {
+            if (!c) return;
+            const uint64_t ns = static_cast<uint64_t>(
+                std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count());
+            ++c->host.calls;
+            c->host.ns += ns;
+            c->host.ns_max = std::max(c->host.ns_max, ns);
+        }
+    } timed{comm, t0};
     return guarded([&] {
         if (!comm || !sendcounts || !sdispls || !recvcounts || !rdispls)
             throw nb::Error(nimbleInvalidArgument, "alltoallv: null argument");
@@ -1560,7 +1653,18 @@ nimbleResult_t nimbleCommGetStats(nimbleComm_t c, nimbleCommStats* out, int rese
         nb::DeviceGuard g(c->device);
         nb::quiesce(c);
         CUDA_TRY(cudaMemcpy(out, c->d_stats, sizeof *out, cudaMemcpyDeviceToHost));
-        if (reset) CUDA_TRY(cudaMemset(c->d_stats, 0, sizeof(nb::DeviceStats)));
+        out->host_calls = c->host.calls;
+        out->host_ns = c->host.ns;
+        out->host_ns_max = c->host.ns_max;
+        out->plans_built = c->host.plans;
+        out->plan_ns = c->host.plan_ns;
+        out->schedules_built = c->host.schedules;
+        out->schedule_ns = c->host.schedule_ns;
+        out->host_pad = 0;
+        if (reset) {
+            CUDA_TRY(cudaMemset(c->d_stats, 0, sizeof(nb::DeviceStats)));
+            c->host = {};
+        }
     });
 }
 

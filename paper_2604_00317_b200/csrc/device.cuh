@@ -177,6 +177,12 @@ struct DeviceStats {
     unsigned long long occ_double;   // claims of a slot still held by an undrained chunk (must stay 0)
     unsigned long long occ_claims;   // ring-slot claims made
     unsigned long long pad;
+    // host side (filled by nimbleCommGetStats, not by the device): the C ABI's
+    // per-call cost -- data-path calls, their total / max wall time, and the
+    // plans and schedules built for new matrices (cache misses)
+    unsigned long long host_calls, host_ns, host_ns_max;
+    unsigned long long plans_built, plan_ns, schedules_built, schedule_ns;
+    unsigned long long host_pad;
 };
 
 // Comm-lifetime device view (set up once at init / registration).
@@ -187,6 +193,8 @@ struct CommDevice {
     uint64_t* win_table;          // [win * kMaxRanks + rank] -> mapped window base
     uint32_t nwin;
     uint32_t timeout_ms;
+    uint32_t ring_full;           // 1: R x R staging rings (mesh model), 0: R self rings indexed by sender
+    uint32_t pad0;
     uint32_t* status;             // host-mapped: [0] error code, [1] detail
     uint64_t* epoch;              // launches completed on this comm (advanced by each launch's last CTA)
     DeviceStats* stats;           // null unless NIMBLE_STATS=1

@@ -353,7 +353,9 @@ __device__ __forceinline__ bool pull_granted_to(const SharedState& sh, const Lau
 
 __device__ __forceinline__ uint8_t* ring_slot(const LaunchArgs& a, int host, int s, int d, uint32_t seq) {
     const int R = a.comm->nranks;
-    const uint64_t ring = static_cast<uint64_t>(s) * R + d;
+    // ring (s, d) hosted on `host`: R x R rings under the mesh model, else only
+    // self rings (host == d), indexed by sender
+    const uint64_t ring = a.comm->ring_full ? static_cast<uint64_t>(s) * R + d : static_cast<uint64_t>(s);
     return a.comm->staging[host] + (ring * a.slots + seq % a.slots) * a.pipe_chunk;
 }
 

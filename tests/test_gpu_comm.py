@@ -145,13 +145,22 @@ def _thread_server(R, conn):
                 _CTX.mode, _CTX.barrier = "thread", barrier
                 s = torch.cuda.Stream()
                 with torch.cuda.stream(s):
+                    comm = None
                     comm = C.Comm.init_rank(R, uid, rank)
                     out[rank] = globals()[fn](comm, rank, R, *args)
                     s.synchronize()
                     barrier.wait(timeout=_CALL_TIMEOUT_S)
                     comm.destroy()
-            except Exception:
-                out[rank] = "ERROR " + traceback.format_exc()
+            except Exception as e:
+                if isinstance(e, threading.BrokenBarrierError):
+                    out[rank] = "ERROR (another rank failed first)"
+                else:
+                    err = ""
+                    try:
+                        err = f" [async error {comm.async_error()}]"
+                    except Exception:
+                        pass
+                    out[rank] = "ERROR" + err + " " + traceback.format_exc()
                 barrier.abort()
 
         threads = [threading.Thread(target=run, args=(r,), daemon=True) for r in range(R)]
@@ -212,7 +221,7 @@ def _threads(fn, R, *args):
     errors = [(r, v) for r, v in enumerate(out) if isinstance(v, str) and v.startswith("ERROR")]
     if errors:
         _kill(R)  # ranks may be stuck in a collective: start over
-        pytest.fail(f"rank {errors[0][0]}: {errors[0][1]}")
+        pytest.fail("\n".join(f"rank {r}: {v}" for r, v in errors))
     return dict(enumerate(out))
 
 

@@ -19,6 +19,7 @@ import time
 
 import torch
 
+os.environ.setdefault("NIMBLE_STATS", "1")  # the comm's host / device counters
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from bench import fresh_matrices  # noqa: E402
@@ -43,6 +44,7 @@ def run_rank(comm, rank, R, args, barrier):
             a, b, c, d = lays[args.calls + k]
             comm.alltoallv(send, a, b, recv, c, d)
         st.synchronize()
+        comm.stats(reset=True)
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         host = []
@@ -54,7 +56,13 @@ def run_rank(comm, rank, R, args, barrier):
             host.append(time.perf_counter() - t0)
         e1.record()
         st.synchronize()
-        out[mode] = {"host_us_median": statistics.median(host) * 1e6, "host_us_p90": sorted(host)[int(0.9 * len(host))] * 1e6,
+        cs = comm.stats()
+        out[mode] = {"python_us_median": statistics.median(host) * 1e6,
+                     "c_abi_us_mean": cs["host_ns"] / max(cs["host_calls"], 1) / 1e3,
+                     "c_abi_us_max": cs["host_ns_max"] / 1e3,
+                     "plans_built": cs["plans_built"], "plan_us_mean": cs["plan_ns"] / max(cs["plans_built"], 1) / 1e3,
+                     "schedules_built": cs["schedules_built"],
+                     "schedule_us_mean": cs["schedule_ns"] / max(cs["schedules_built"], 1) / 1e3,
                      "device_ms_per_call": e0.elapsed_time(e1) / args.calls}
         barrier()
     comm.check_async()
