@@ -235,10 +235,12 @@ nimbleResult_t nimbleCommDeregister(const nimbleComm_t comm, void* handle);
 nimbleResult_t nimbleMemAlloc(void** ptr, size_t size);
 nimbleResult_t nimbleMemFree(void* ptr);
 
-/* Group semantics follow NCCL (ops are enqueued, one exchange per comm is
- * launched at GroupEnd), with one restriction: a group may hold at most one
- * send to and one receive from each peer (each pair is one contiguous
- * segment); a second one is an nimbleInvalidUsage error, not a queued op. */
+/* Group semantics follow NCCL: ops are enqueued and one exchange per comm is
+ * launched at GroupEnd.  Several sends to (receives from) one peer in a group
+ * are matched in issue order with the peer's receives (sends), each pair of
+ * matching operations having the same byte count (ncclSend / ncclRecv
+ * rules); such a pair is pushed through the receiver's staging ring and
+ * drained into each receive buffer in turn (nvswitch model only). */
 nimbleResult_t nimbleGroupStart(void);
 nimbleResult_t nimbleGroupEnd(void);
 nimbleResult_t nimbleSend(const void* sendbuff, size_t count, nimbleDataType_t datatype, int peer,

@@ -616,30 +616,47 @@ Exchange make_exchange(nimbleComm* c, const std::vector<PendingOp*>& ops) {
     ex.rb.recv_bytes.assign(R, 0);
     ex.has_send.assign(R, false);
     ex.has_recv.assign(R, false);
-    auto set_send = [&](int p, uint64_t ptr, uint64_t n) {
-        if (ex.has_send[p]) throw Error(nimbleInvalidUsage, "group: two sends to one peer");
-        ex.has_send[p] = true;
-        ex.rb.send_ptr[p] = ptr;
-        ex.rb.send_bytes[p] = n;
-    };
-    auto set_recv = [&](int p, uint64_t ptr, uint64_t n) {
-        if (ex.has_recv[p]) throw Error(nimbleInvalidUsage, "group: two receives from one peer");
-        ex.has_recv[p] = true;
-        ex.rb.recv_ptr[p] = ptr;
-        ex.rb.recv_bytes[p] = n;
-    };
+    // NCCL group semantics: several sends to (receives from) one peer are
+    // matched in issue order with the peer's receives (sends); the pair then
+    // consists of those parts, in that order
+    std::vector<std::vector<std::pair<uint64_t, uint64_t>>> sends(static_cast<size_t>(R)), recvs(static_cast<size_t>(R));
     for (PendingOp* op : ops) {
         if (op->stream != ex.stream &&
             std::find(ex.others.begin(), ex.others.end(), op->stream) == ex.others.end())
             ex.others.push_back(op->stream);
-        if (op->kind == PendingOp::Send) set_send(op->peer, op->ptr, op->bytes);
-        else if (op->kind == PendingOp::Recv) set_recv(op->peer, op->ptr, op->bytes);
+        if (op->kind == PendingOp::Send) sends[static_cast<size_t>(op->peer)].push_back({op->ptr, op->bytes});
+        else if (op->kind == PendingOp::Recv) recvs[static_cast<size_t>(op->peer)].push_back({op->ptr, op->bytes});
         else
             for (int p = 0; p < R; ++p) {
-                set_send(p, op->sbase + op->soff[p], op->sbytes[p]);
-                set_recv(p, op->rbase + op->roff[p], op->rbytes[p]);
+                sends[static_cast<size_t>(p)].push_back({op->sbase + op->soff[p], op->sbytes[p]});
+                recvs[static_cast<size_t>(p)].push_back({op->rbase + op->roff[p], op->rbytes[p]});
             }
     }
+    auto settle = [&](std::vector<std::pair<uint64_t, uint64_t>>& parts, std::vector<bool>& has,
+                      std::vector<uint64_t>& ptr, std::vector<uint64_t>& bytes,
+                      std::vector<std::vector<std::pair<uint64_t, uint64_t>>>& multi, int p) {
+        if (parts.empty()) return;
+        has[static_cast<size_t>(p)] = true;
+        if (parts.size() > 1)  // zero-byte operations carry nothing (both ends drop them alike)
+            parts.erase(std::remove_if(parts.begin(), parts.end(), [](const auto& x) { return x.second == 0; }),
+                        parts.end());
+        if (parts.empty()) return;
+        ptr[static_cast<size_t>(p)] = parts[0].first;
+        uint64_t total = 0;
+        for (const auto& x : parts) total += x.second;
+        bytes[static_cast<size_t>(p)] = total;
+        if (parts.size() > 1) {
+            if (p == c->rank) throw Error(nimbleInvalidUsage, "group: several operations on the self segment");
+            if (multi.empty()) multi.resize(static_cast<size_t>(R));
+            multi[static_cast<size_t>(p)] = parts;
+        }
+    };
+    for (int p = 0; p < R; ++p) {
+        settle(sends[static_cast<size_t>(p)], ex.has_send, ex.rb.send_ptr, ex.rb.send_bytes, ex.rb.send_parts, p);
+        settle(recvs[static_cast<size_t>(p)], ex.has_recv, ex.rb.recv_ptr, ex.rb.recv_bytes, ex.rb.recv_parts, p);
+    }
+    if ((!ex.rb.send_parts.empty() || !ex.rb.recv_parts.empty()) && c->cfg.fabric == nimbleFabricAllToAll)
+        throw Error(nimbleInvalidUsage, "group: several operations per peer need the nvswitch model");
     return ex;
 }
 
@@ -689,12 +706,14 @@ void fill_posts(nimbleComm* c, RankBuffers& rb, const PlanResult& plan) {
     rb.send_post.assign(static_cast<size_t>(rb.R), Post{});
     const uint64_t ll_max = c->cfg.ll_max;
     for (int d = 0; d < rb.R; ++d) {
-        if (d == rb.me || rb.send_bytes[d] == 0 || ll_pair(plan, rb.me, d, rb.send_bytes[d], ll_max)) continue;
+        const bool several = pair_is_multi(rb, rb.me, d);
+        if (d == rb.me || rb.send_bytes[d] == 0 || (!several && ll_pair(plan, rb.me, d, rb.send_bytes[d], ll_max)))
+            continue;
         Post p{};
         p.tag = 1;
         p.bytes = rb.send_bytes[d];
         p.mode = kSendPlain;
-        const int w = window_of(c, rb.send_ptr[d], rb.send_bytes[d]);
+        const int w = several ? -1 : window_of(c, rb.send_ptr[d], rb.send_bytes[d]);
         if (w >= 0 && grant) {
             p.mode = kSendRegistered;
             p.win = static_cast<uint32_t>(w);
@@ -710,12 +729,18 @@ void fill_posts(nimbleComm* c, RankBuffers& rb, const PlanResult& plan) {
             for (const Flow& f : pr.flows) relayed[static_cast<size_t>(pr.src)] |= pr.cands[static_cast<size_t>(f.cand)].via >= 0;
     rb.recv_post.assign(static_cast<size_t>(rb.R), Post{});
     for (int s = 0; s < rb.R; ++s) {
-        if (s == rb.me || rb.recv_bytes[s] == 0 || ll_pair(plan, s, rb.me, rb.recv_bytes[s], ll_max)) continue;
+        const bool several = pair_is_multi(rb, s, rb.me);
+        if (s == rb.me || rb.recv_bytes[s] == 0 || (!several && ll_pair(plan, s, rb.me, rb.recv_bytes[s], ll_max)))
+            continue;
         Post p{};
         p.tag = 1;
         p.bytes = rb.recv_bytes[s];
         p.mode = kPostStaged;
-        p.off = rb.recv_ptr[s];
+        p.off = several ? 0 : rb.recv_ptr[s];  // several parts: the drain items carry absolute addresses
+        if (several) {
+            rb.recv_post[static_cast<size_t>(s)] = p;
+            continue;
+        }
         const int w = window_of(c, rb.recv_ptr[s], rb.recv_bytes[s]);
         if (w >= 0) {
             p.mode = kPostZeroCopy;
@@ -770,6 +795,15 @@ CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& 
         key.push_back(rb.recv_post[r].win);
         key.push_back(rb.send_post[r].mode);
         key.push_back(rb.send_post[r].win);
+    }
+    for (const auto* parts : {&rb.send_parts, &rb.recv_parts}) {
+        key.push_back(~0ull);  // list separator
+        for (size_t p = 0; p < parts->size(); ++p)
+            for (const auto& [ptr, bytes] : (*parts)[p]) {
+                key.push_back(p);
+                key.push_back(ptr);
+                key.push_back(bytes);
+            }
     }
     for (auto it = c->schedules.begin(); it != c->schedules.end(); ++it)
         if (it->key == key) {
@@ -1395,6 +1429,14 @@ nimbleResult_t nimbleCommGetAsyncError(nimbleComm_t c, nimbleResult_t* err) {
                                      "a post was overwritten before it was read (protocol violation)",
                                      "timeout on a low-latency (LL) slot"};
         nb::g_last_error = code < sizeof what / sizeof what[0] ? what[code] : "unknown device error";
+        // where: peer (0xff = unknown; bit 7 = the other direction: a pull, or
+        // an LL receive) and the epoch's low 16 bits
+        const uint32_t detail = reinterpret_cast<volatile uint32_t*>(c->h_status)[1];
+        const uint32_t peer = detail >> 16 & 0xff;
+        nb::g_last_error += " (rank " + std::to_string(c->rank) + ", peer " +
+                            (peer == 0xff ? std::string("?") : std::to_string(peer & 0x7f) +
+                                                                   ((peer & 0x80) ? " [in]" : "")) +
+                            ", epoch " + std::to_string(detail & 0xffff) + ")";
     }
     return nimbleSuccess;
 }

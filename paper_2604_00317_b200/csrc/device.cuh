@@ -62,10 +62,12 @@ struct Item {
 static_assert(sizeof(Item) == 32, "Item layout");
 
 // One flow of a rank's chunk schedule (schedule.cpp): item k covers bytes
-// [k * chunk, min((k + 1) * chunk, bytes)) of the flow and sorts by the key
-// (k + 0.5) / n + phase -- its progress fraction -- ties going to the larger
+// [k * chunk, min((k + 1) * chunk, bytes)) of the flow, carries chunk index
+// proto.seq + k, and sorts by the key (k + 0.5) / n * scale + phase -- its
+// progress fraction (scale 1 except for the parts of a pair built from
+// several sends, which share the pair's progress) -- ties going to the larger
 // flow, then to the earlier insertion index base + k.  The host merges the
-// flows into the item list (schedule.cpp, ordered) or the device does
+// flows into the item list (schedule.cpp, merge_cuts) or the device does
 // (engine.cu, gen_items_kernel) -- identical lists either way.
 enum CutFlags : uint32_t { kCutSrc = 1, kCutDst = 2, kCutPull = 4 };
 struct CutDesc {
@@ -73,11 +75,11 @@ struct CutDesc {
     uint64_t src0, dst0;    // item k: src = src0 + k * chunk (kCutSrc), dst = dst0 + k * chunk (kCutDst)
     uint64_t bytes, chunk, n;
     uint64_t src_from_dst;  // kCutPull: src = dst - src_from_dst (offset inside the sender's segment)
-    double phase;
+    double phase, scale;
     uint32_t base;          // insertion index of item 0
     uint32_t flags;         // CutFlags
 };
-static_assert(sizeof(CutDesc) == 96, "CutDesc layout");
+static_assert(sizeof(CutDesc) == 104, "CutDesc layout");
 
 // Receive posts: where a sender's segment lands (+ a pull request bit).
 // Send posts: where my outgoing segment lives, if it is registered.

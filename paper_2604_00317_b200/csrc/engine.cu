@@ -143,9 +143,18 @@ enum AsyncCode : uint32_t {
     kErrLLTimeout = 9,   // an LL slot never filled (or its receiver never drained the previous one)
 };
 
+// Latch the first async error of the comm: status[0] = code, status[1] =
+// where (peer << 16 | low 16 bits of the epoch), for nimbleCommGetAsyncError.
+__device__ __forceinline__ void latch(const CommDevice* c, uint32_t code, uint32_t peer = 0xff, uint64_t epoch = 0) {
+    if (atomicCAS(c->status, 0u, code) == 0u) {
+        c->status[1] = (peer & 0xffu) << 16 | static_cast<uint32_t>(epoch & 0xffffu);
+        __threadfence_system();
+    }
+}
+
 // Producer-thread wait until *p >= tag; false (and an async error) on timeout
 // or when another wait already failed.
-__device__ bool wait_ge(const uint64_t* p, uint64_t tag, const CommDevice* c, uint32_t code) {
+__device__ bool wait_ge(const uint64_t* p, uint64_t tag, const CommDevice* c, uint32_t code, uint32_t peer = 0xff) {
     if (ld_acquire(p) >= tag) return true;
     const uint64_t t0 = global_ns();
     const uint64_t limit = static_cast<uint64_t>(c->timeout_ms) * 1000000ull;
@@ -155,7 +164,7 @@ __device__ bool wait_ge(const uint64_t* p, uint64_t tag, const CommDevice* c, ui
         if ((spin & 255) == 255) {
             if (*status != 0) return false;
             if (global_ns() - t0 > limit) {
-                atomicCAS(c->status, 0u, code);
+                latch(c, code, peer, tag >> 32 ? tag >> 32 : tag);
                 return false;
             }
         }
@@ -262,7 +271,7 @@ __device__ PostRead read_post(const WirePost* p, uint64_t epoch, const CommDevic
         if ((spin & 255) == 255) {
             if (*reinterpret_cast<volatile uint32_t*>(c->status) != 0) return kPostFailed;
             if (global_ns() - t0 > limit) {
-                atomicCAS(c->status, 0u, static_cast<uint32_t>(kErrPostTimeout));
+                latch(c, kErrPostTimeout, 0xff, epoch);
                 return kPostFailed;
             }
         }
@@ -507,7 +516,7 @@ __device__ void ll_send_all(const LaunchArgs& a) {
         const int d = it.peer;
         if (threadIdx.x == 0) {
             const CtrlHeader* h = reinterpret_cast<const CtrlHeader*>(c->ctrl[me]);
-            ok = a.epoch <= 2 || wait_ge(&h->ll_ack[d], a.epoch - 2, c, kErrLLTimeout);
+            ok = a.epoch <= 2 || wait_ge(&h->ll_ack[d], a.epoch - 2, c, kErrLLTimeout, static_cast<uint32_t>(d));
         }
         __syncthreads();
         if (ok) {
@@ -560,7 +569,7 @@ __device__ void ll_recv_all(const LaunchArgs& a) {
                     if ((spin & 255) == 255) {
                         if (*status != 0) break;
                         if (global_ns() - t0 > limit) {
-                            atomicCAS(c->status, 0u, static_cast<uint32_t>(kErrLLTimeout));
+                            latch(c, kErrLLTimeout, 0x80u | static_cast<uint32_t>(s), a.epoch);
                             break;
                         }
                     }
@@ -900,9 +909,9 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
                 bool need_done = (a.relay_writers >> w) & 1;
                 if (((a.recv_direct >> w) & 1) && ((a.recv_zc >> w) & 1))  // w pushed in place unless I pulled
                     need_done |= !(((a.pull_req >> w) & 1) && decide[kMaxRanks + w] == kDecidePull);
-                if (need_done) wait_ge(&h->done[w], done_tag, c, kErrDoneTimeout);
+                if (need_done) wait_ge(&h->done[w], done_tag, c, kErrDoneTimeout, static_cast<uint32_t>(w));
                 if (((a.push_targets >> w) & 1) && decide[w] == kDecidePull)  // w pulled my segment
-                    wait_ge(&h->pulled[w], done_tag, c, kErrDoneTimeout);
+                    wait_ge(&h->pulled[w], done_tag, c, kErrDoneTimeout, 0x80u | static_cast<uint32_t>(w));
             }
             __syncwarp();
         }
@@ -930,7 +939,7 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
 // no contraction), so the list is the host's, item for item.
 
 __device__ __forceinline__ double gen_key(const CutDesc& f, uint64_t k) {
-    return __dadd_rn(__ddiv_rn(static_cast<double>(k) + 0.5, static_cast<double>(f.n)), f.phase);
+    return __dadd_rn(__dmul_rn(__ddiv_rn(static_cast<double>(k) + 0.5, static_cast<double>(f.n)), f.scale), f.phase);
 }
 
 __device__ __forceinline__ bool gen_before(const CutDesc& a, uint64_t ka, double keya, const CutDesc& b, uint64_t kb,
@@ -946,7 +955,7 @@ __device__ __forceinline__ Item gen_item(const CutDesc& f, uint64_t k) {
     it.src = (f.flags & kCutSrc) ? f.src0 + off : 0;
     it.dst = (f.flags & kCutDst) ? f.dst0 + off : 0;
     it.bytes = static_cast<uint32_t>(f.chunk < f.bytes - off ? f.chunk : f.bytes - off);
-    it.seq = static_cast<uint32_t>(k);
+    it.seq = f.proto.seq + static_cast<uint32_t>(k);
     if (f.flags & kCutPull) it.src = it.dst - f.src_from_dst;
     return it;
 }
@@ -985,8 +994,8 @@ __global__ void __launch_bounds__(256) gen_items_kernel(const __grid_constant__ 
                 pos += k;
                 continue;
             }
-            // guess: k' with (k' + 0.5) / n + phase < key, then settle exactly
-            const double x = (key - c.phase) * static_cast<double>(c.n) - 0.5;
+            // guess: k' with (k' + 0.5) / n * scale + phase < key, then settle exactly
+            const double x = (key - c.phase) / c.scale * static_cast<double>(c.n) - 0.5;
             int64_t q = x <= 0.0 ? 0 : (x >= static_cast<double>(c.n) ? static_cast<int64_t>(c.n) : static_cast<int64_t>(ceil(x)));
             while (q < static_cast<int64_t>(c.n) && gen_before(c, q, gen_key(c, q), f, k, key)) ++q;
             while (q > 0 && !gen_before(c, q - 1, gen_key(c, q - 1), f, k, key)) --q;

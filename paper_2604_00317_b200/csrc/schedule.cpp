@@ -17,7 +17,7 @@ struct Cuts {
 
 // Appends one flow (device.cuh CutDesc); returns its item count.
 uint32_t cut(Cuts& out, Item proto, uint64_t src0, uint64_t dst0, uint64_t bytes, uint64_t chunk, double phase,
-             bool pull = false, uint64_t src_from_dst = 0) {
+             bool pull = false, uint64_t src_from_dst = 0, double scale = 1.0) {
     const uint64_t n = (bytes + chunk - 1) / chunk;
     if (n) {
         CutDesc c{};
@@ -29,6 +29,7 @@ uint32_t cut(Cuts& out, Item proto, uint64_t src0, uint64_t dst0, uint64_t bytes
         c.n = n;
         c.src_from_dst = src_from_dst;
         c.phase = phase;
+        c.scale = scale;
         c.base = out.count;
         c.flags = (src0 ? static_cast<uint32_t>(kCutSrc) : 0u) | kCutDst | (pull ? static_cast<uint32_t>(kCutPull) : 0u);
         out.flows.push_back(c);
@@ -58,13 +59,13 @@ Item cut_item(const CutDesc& f, uint64_t k) {
     it.src = (f.flags & kCutSrc) ? f.src0 + off : 0;
     it.dst = (f.flags & kCutDst) ? f.dst0 + off : 0;
     it.bytes = static_cast<uint32_t>(std::min(f.chunk, f.bytes - off));
-    it.seq = static_cast<uint32_t>(k);
+    it.seq = f.proto.seq + static_cast<uint32_t>(k);
     if (f.flags & kCutPull) it.src = it.dst - f.src_from_dst;
     return it;
 }
 
 double cut_key(const CutDesc& f, uint64_t k) {
-    return (static_cast<double>(k) + 0.5) / static_cast<double>(f.n) + f.phase;
+    return (static_cast<double>(k) + 0.5) / static_cast<double>(f.n) * f.scale + f.phase;
 }
 
 // All items in `before` order: a k-way merge over the flows (each one's keys
@@ -107,7 +108,33 @@ namespace {
 
 constexpr double kHop2 = 1e-9;  // forward of chunk k sorts right after its stage-in
 
+// A pair made of several group operations (NCCL: several sends to, or
+// receives from, one peer in a group, matched in order).
+bool multi(const std::vector<std::vector<std::pair<uint64_t, uint64_t>>>& parts, int peer) {
+    return static_cast<size_t>(peer) < parts.size() && parts[static_cast<size_t>(peer)].size() > 1;
+}
+
+// Each part (ptr, offset inside the pair, bytes, first chunk index).
+template <typename F>
+void each_part(const std::vector<std::pair<uint64_t, uint64_t>>& parts, uint64_t chunk, F&& f) {
+    uint64_t off = 0;
+    uint32_t seq = 0;
+    for (const auto& [ptr, bytes] : parts) {
+        f(ptr, off, bytes, seq);
+        off += bytes;
+        seq += static_cast<uint32_t>((bytes + chunk - 1) / chunk);
+    }
+}
+
+// part keys span [off / total, (off + bytes) / total): the pair's progress
+double part_phase(uint64_t off, uint64_t total) { return static_cast<double>(off) / static_cast<double>(total); }
+double part_scale(uint64_t bytes, uint64_t total) { return static_cast<double>(bytes) / static_cast<double>(total); }
+
 }  // namespace
+
+bool pair_is_multi(const RankBuffers& rb, int s, int d) {
+    return s == rb.me ? multi(rb.send_parts, d) : d == rb.me ? multi(rb.recv_parts, s) : false;
+}
 
 bool ll_pair(const PlanResult& plan, int s, int d, uint64_t bytes, uint64_t ll_max) {
     if (s == d || bytes == 0 || bytes > ll_max || bytes > kLLMaxData) return false;
@@ -147,7 +174,7 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
     Cuts ll_send, ll_recv;
     for (const PairRoutes& pr : plan.pairs) {
         const int s = pr.src, d = pr.dst;
-        if ((s == me || d == me) && ll_pair(plan, s, d, pr.demand, ll_max)) {
+        if ((s == me || d == me) && !pair_is_multi(rb, s, d) && ll_pair(plan, s, d, pr.demand, ll_max)) {
             if (s == me && pr.demand != rb.send_bytes[d])
                 throw Error(nimbleInvalidArgument, "schedule: plan demand differs from the send count");
             if (d == me && pr.demand != rb.recv_bytes[s])
@@ -187,7 +214,23 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
             if (static_cast<double>(bytes) != f.bytes) throw Error(nimbleInternalError, "schedule: fractional flow");
             if (c.route == Route::Rail) throw Error(nimbleInvalidUsage, "schedule: inter-node rail routes need a multi-node box");
             if (c.route == Route::Direct) {
-                if (s == me) {
+                if (s == me && multi(rb.send_parts, d)) {
+                    // several sends to d in one group: one cut per part, chunk
+                    // indices and progress keys continuing across the parts
+                    // (the receiver cuts its receives identically)
+                    if (bytes != pr.demand) throw Error(nimbleInvalidUsage, "group: several sends to one peer need a direct route");
+                    Item proto{};
+                    proto.kind = kPush;
+                    proto.peer = static_cast<uint8_t>(d);
+                    each_part(rb.send_parts[d], schunk, [&](uint64_t ptr, uint64_t po, uint64_t pb, uint32_t seq0) {
+                        proto.seq = seq0;
+                        sc.push_items[d] += cut(keyed, proto, ptr, po, pb, schunk, part_phase(po, pr.demand), false, 0,
+                                                part_scale(pb, pr.demand));
+                    });
+                    sc.push_targets |= 1ull << d;
+                    sc.write_targets |= 1ull << d;
+                    sc.moved_bytes += bytes;
+                } else if (s == me) {
                     Item proto{};
                     proto.kind = kPush;
                     proto.peer = static_cast<uint8_t>(d);
@@ -196,7 +239,21 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
                     sc.write_targets |= 1ull << d;
                     sc.moved_bytes += bytes;
                 }
-                if (d == me) {
+                if (d == me && multi(rb.recv_parts, s)) {
+                    // several receives from s: staged through my self ring,
+                    // each part drained to its own buffer (absolute addresses)
+                    if (bytes != pr.demand) throw Error(nimbleInvalidUsage, "group: several receives from one peer need a direct route");
+                    sc.recv_direct |= 1ull << s;
+                    Item proto{};
+                    proto.kind = kForward;
+                    proto.peer = static_cast<uint8_t>(me);
+                    proto.aux = static_cast<uint16_t>(s);
+                    each_part(rb.recv_parts[s], schunk, [&](uint64_t ptr, uint64_t po, uint64_t pb, uint32_t seq0) {
+                        proto.seq = seq0;
+                        cut(keyed, proto, 0, ptr, pb, schunk, part_phase(po, pr.demand) + kHop2, false, 0,
+                            part_scale(pb, pr.demand));
+                    });
+                } else if (d == me) {
                     sc.recv_direct |= 1ull << s;
                     if (rb.recv_post[s].mode & kPostPullRequest) {  // used if the sender grants it at run time
                         sc.pull_req |= 1ull << s;

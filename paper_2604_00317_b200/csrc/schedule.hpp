@@ -29,6 +29,9 @@ struct RankBuffers {
     std::vector<Post> recv_post;                 // [R] mode/win/off per sender (tag != 0: present)
     std::vector<Post> send_post;                 // [R] registered window of each outgoing segment
     bool pull = false;                           // ask senders to let me pull my direct flows
+    // [R] pairs built from several group operations: (ptr, bytes) per
+    // operation, in issue order (empty or one entry: a plain segment)
+    std::vector<std::vector<std::pair<uint64_t, uint64_t>>> send_parts, recv_parts;
 };
 
 struct Schedule {
@@ -64,6 +67,11 @@ double cut_key(const CutDesc& f, uint64_t k);
 std::vector<Item> merge_cuts(const std::vector<CutDesc>& flows);
 // Fill sc.items / sc.ll_items on the host from the cuts.
 void materialize(Schedule& sc);
+
+// Is pair (s, d), one end of which is me, built from several group
+// operations?  (Never LL, never pulled or zero copy: pushed into the
+// receiver's self ring and drained part by part.)
+bool pair_is_multi(const RankBuffers& rb, int s, int d);
 
 // Does pair (s, d) of `bytes` ride the LL protocol?  Both endpoints decide
 // alike from what they both know: the pair size and the replicated plan

@@ -996,3 +996,76 @@ def test_moe_custom_op_forward_and_gradients(layout):
 def test_stress_ll_and_normal_pairs_back_to_back(layout):
     out = _run(layout, "w_stress_ll")
     assert all(v == 0 for v in out.values()), out
+
+
+def w_sendrecv_multi(comm, rank, R):
+    """NCCL group semantics: several sends to one peer and several receives
+    from one peer in one group, matched in issue order (odd sizes, a zero-byte
+    operation in between, one part above the LL limit), next to a plain pair;
+    each receive buffer holds exactly its part of the pair's payload."""
+    from paper_2604_00317_b200 import comm as C
+    right, left = (rank + 1) % R, (rank - 1) % R
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for it, sizes in enumerate([[3, 0, 70001, 8192], [(1 << 20) + 5, 77, 2 * MiB + 3], [1, 2, 3, 4, 5]]):
+        xs, ys, off = [], [], 0
+        for n in sizes:
+            x = torch.empty(max(n, 1), dtype=torch.uint8, device="cuda")
+            C.fill_payload(x, off, n, 700 + it, rank, right)
+            xs.append((x, n, off))
+            ys.append((torch.zeros(max(n, 1), dtype=torch.uint8, device="cuda"), n, off))
+            off += n
+        one = 5 * MiB + 1
+        z = torch.empty(one, dtype=torch.uint8, device="cuda")
+        C.fill_payload(z, 0, one, 800 + it, rank, (rank + 2) % R)
+        zr = torch.zeros(one, dtype=torch.uint8, device="cuda")
+        with C.group():
+            for x, n, _ in xs:
+                comm.send(x, n, right)
+            for y, n, _ in ys:
+                comm.recv(y, n, left)
+            if R > 2:
+                comm.send(z, one, (rank + 2) % R)
+                comm.recv(zr, one, (rank - 2) % R)
+        _sync()
+        comm.check_async()
+        for y, n, o in ys:
+            C.check_payload(y, o, n, 700 + it, left, rank, bad)
+        if R > 2:
+            C.check_payload(zr, 0, one, 800 + it, (rank - 2) % R, rank, bad)
+    _sync()
+    return int(bad.item())
+
+
+@pytest.mark.parametrize("layout", _layouts(2, 4))
+def test_sendrecv_several_ops_per_peer(layout):
+    out = _run(layout, "w_sendrecv_multi")
+    assert all(v == 0 for v in out.values()), out
+
+
+def w_moe_counts(comm, rank, R):
+    """The MoE dispatch's count exchange alone (alltoall of one int64 per
+    peer) and its row exchange sizes: returns (count_out, count_in)."""
+    from paper_2604_00317_b200.moe import MoEDispatcher
+    g = torch.Generator(device="cuda").manual_seed(100 + rank)
+    T, H, k, E = 777, 96, 2, 4 * R
+    x = torch.randn(T, H, device="cuda", generator=g)
+    hot = torch.rand(T, k, device="cuda", generator=g) < 0.6
+    ids = torch.where(hot, torch.zeros_like(hot, dtype=torch.int64),
+                      torch.randint(0, E, (T, k), device="cuda", generator=g))
+    disp = MoEDispatcher(comm, E, H, dtype=torch.float32, max_tokens=1024, topk=k)
+    try:
+        recv_x, recv_e, h = disp.dispatch(x, ids)
+        _sync()
+        comm.check_async()
+        return list(h.send_counts), list(h.recv_counts)
+    finally:
+        disp.close()
+
+
+@pytest.mark.parametrize("layout", _layouts(2, 4))
+def test_moe_count_exchange_consistent(layout):
+    out = _run(layout, "w_moe_counts")
+    R = len(out)
+    for r in range(R):
+        for s in range(R):
+            assert out[r][1][s] == out[s][0][r], (r, s, out)

@@ -58,6 +58,23 @@ def timed(fn, st, iters, warmup):
     return v[len(v) // 2], v[0], sum(v) / len(v)
 
 
+def nvml_read():
+    """NVLink byte counters of this rank's GPU (SWEEP_NVML=1), else None."""
+    if os.environ.get("SWEEP_NVML") != "1":
+        return None
+    try:
+        from tools import nvml_nvlink
+        return nvml_nvlink.read(torch.cuda.current_device())
+    except Exception as e:  # driver without the counters
+        return {"error": str(e)[:80]}
+
+
+def nvml_delta(a, b, calls):
+    if a is None or b is None or "error" in a or "error" in b:
+        return a if a and "error" in a else None
+    return {k: (b[k] - a[k]) / calls if a[k] is not None and b[k] is not None else None for k in a}
+
+
 def timed_graph(fn, st, iters, warmup):
     """`iters` calls captured in one CUDA graph, replayed once: per-call device
     time without host launch overhead (max over ranks).  Returns seconds."""
@@ -89,7 +106,9 @@ def _run_point(comm, pg, rank, R, m, name, fabric="nvswitch", iters=None, warmup
         C.fill_payload(send[sd[d]:], 0, sc[d], 9, rank, d)
     hs, hr = comm.register(send), comm.register(recv)
     st = torch.cuda.current_stream()
+    nvl0 = nvml_read()
     t, t_min, t_mean = timed(lambda: comm.alltoallv(send, sc, sd, recv, rc, rd, st), st, iters, warmup)
+    nvl = nvml_delta(nvl0, nvml_read(), iters + warmup)
     comm.check_async()
     bad = torch.zeros(1, dtype=torch.int64, device="cuda")
     for s in range(R):
@@ -125,6 +144,11 @@ def _run_point(comm, pg, rank, R, m, name, fabric="nvswitch", iters=None, warmup
            "vs_nccl": (tn / t) if tn else None, "relay_flows": relays, "mismatched_bytes": mism}
     if graph:
         row["graph"] = graph
+    if nvl is not None:  # this rank's NVLink counters per call (rank 0 prints its own; hot rank = 0)
+        row["nvlink_per_call_rank0"] = nvl
+        sent = sum(m[rank * R + d] for d in range(R) if d != rank)
+        got = sum(m[s * R + rank] for s in range(R) if s != rank)
+        row["payload_per_call_rank0"] = {"egress": sent, "ingress": got}
     if extra:
         row.update(extra)
     if rank == 0:
