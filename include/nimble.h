@@ -299,6 +299,13 @@ nimbleResult_t nimbleBenchMatrix(nimbleComm_t comm, const uint64_t* matrix, int 
 nimbleResult_t nimbleBootstrapAllgather(const nimbleUniqueId* id, int rank, int nranks, const void* in, size_t n,
                                         void* out);
 
+/* Host-only: the host shared-memory allgather communicators use for per-call
+ * metadata (the mesh model's demand rows), `rounds` times back to back; every
+ * round checks that each record is that round's, from its rank.  `out` gets
+ * the last round's records (nranks * n bytes, n <= 248). */
+nimbleResult_t nimbleBootstrapShmAllgather(const nimbleUniqueId* id, int rank, int nranks, const void* in, size_t n,
+                                           void* out, int rounds);
+
 /* The chunk scheduler, host only: the ordered work items rank `rank` would
  * run for `plan` (from nimblePlanCreate / nimblePlanDirect over `ranks` ranks,
  * packed layout).  recv_staged_mask bit s: my receive segment from s is not

@@ -129,6 +129,7 @@ SIGNATURES = {
     "nimbleBenchSkewed": [c_void_p, c_u64, c_double, c_int, c_int, c_int, P(BenchResult)],
     "nimbleBenchMatrix": [c_void_p, P(c_u64), c_int, c_int, P(BenchResult)],
     "nimbleBootstrapAllgather": [P(UniqueId), c_int, c_int, c_void_p, c_size, c_void_p],
+    "nimbleBootstrapShmAllgather": [P(UniqueId), c_int, c_int, c_void_p, c_size, c_void_p, c_int],
     "nimbleCommDebugTrace": [c_void_p, P(c_u64), c_int],
     "nimbleCommGetStats": [c_void_p, P(CommStats), c_int],
     "nimbleDebugSchedule": [c_void_p, c_int, c_int, c_u64, ctypes.c_uint32, c_u64, c_u64, c_u64, c_u64, c_void_p, c_int,

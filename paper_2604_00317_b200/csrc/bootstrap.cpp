@@ -5,9 +5,12 @@
 #include <netinet/in.h>
 #include <netinet/tcp.h>
 #include <poll.h>
+#include <sys/mman.h>
 #include <sys/socket.h>
+#include <fcntl.h>
 #include <unistd.h>
 
+#include <atomic>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -215,6 +218,68 @@ void bootstrap_root(nimbleUniqueId* id) {
     std::memset(id, 0, sizeof *id);
     std::memcpy(id->internal, &blob, sizeof blob);
     std::thread(serve, lfd, nonce).detach();
+}
+
+// One rank's record, double-buffered by call parity: a writer can be at most
+// one call ahead of the slowest reader (it cannot finish call k + 1 before
+// every rank has written k + 1, i.e. finished reading k).
+struct ShmAllgather::Slot {
+    std::atomic<uint64_t> seq[2];
+    uint8_t data[2][kRecord];
+};
+
+ShmAllgather::ShmAllgather(const nimbleUniqueId& id, Bootstrap& boot) : rank_(boot.rank), nranks_(boot.nranks) {
+    IdBlob blob;
+    std::memcpy(&blob, id.internal, sizeof blob);
+    char name[64];
+    std::snprintf(name, sizeof name, "/nimble-%016llx-%04x", static_cast<unsigned long long>(blob.nonce),
+                  static_cast<unsigned>(blob.port));
+    bytes_ = sizeof(Slot) * static_cast<size_t>(nranks_);
+    if (rank_ == 0) {
+        int fd = ::shm_open(name, O_CREAT | O_EXCL | O_RDWR, 0600);
+        if (fd < 0) sys_fail("shm_open");
+        if (::ftruncate(fd, static_cast<off_t>(bytes_)) != 0) {
+            ::close(fd);
+            ::shm_unlink(name);
+            sys_fail("ftruncate");
+        }
+        ::close(fd);  // zero-filled: every seq starts at 0
+    }
+    boot.barrier();
+    int fd = ::shm_open(name, O_RDWR, 0600);
+    if (fd < 0) sys_fail("shm_open");
+    void* p = ::mmap(nullptr, bytes_, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    ::close(fd);
+    if (p == MAP_FAILED) sys_fail("mmap");
+    slots_ = static_cast<Slot*>(p);
+    boot.barrier();
+    if (rank_ == 0) ::shm_unlink(name);  // the mappings stay; no file outlives the comm
+}
+
+ShmAllgather::~ShmAllgather() {
+    if (slots_) ::munmap(slots_, bytes_);
+}
+
+void ShmAllgather::allgather(const void* mine, size_t n, void* all, uint32_t timeout_ms) {
+    if (n > kRecord) throw Error(nimbleInternalError, "shm allgather: record too large");
+    const uint64_t k = ++calls_;
+    const int par = static_cast<int>(k & 1);
+    Slot& me = slots_[rank_];
+    std::memcpy(me.data[par], mine, n);
+    me.seq[par].store(k, std::memory_order_release);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int r = 0; r < nranks_; ++r) {
+        Slot& s = slots_[r];
+        for (uint32_t spin = 0; s.seq[par].load(std::memory_order_acquire) < k; ++spin) {
+            if (spin > 1000) {
+                std::this_thread::yield();
+                if ((spin & 1023) == 0 &&
+                    std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(timeout_ms))
+                    throw Error(nimbleRemoteError, "shm allgather: a rank did not arrive");
+            }
+        }
+        std::memcpy(static_cast<uint8_t*>(all) + static_cast<size_t>(r) * n, s.data[par], n);
+    }
 }
 
 std::unique_ptr<Bootstrap> bootstrap_connect(const nimbleUniqueId& id, int rank, int nranks) {

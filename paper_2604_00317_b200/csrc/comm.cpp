@@ -263,6 +263,7 @@ struct nimbleComm {
     // sms_share CTAs by default
     int colocated = 1, sms_share = 148;
     std::unique_ptr<nb::Bootstrap> boot;
+    std::unique_ptr<nb::ShmAllgather> shm;  // per-call metadata between ranks (mesh model rows)
     std::shared_ptr<nb::Clique> clique;
     nimbleCommConfig cfg{};
     uint8_t* ctrl = nullptr;
@@ -294,6 +295,11 @@ struct nimbleComm {
     nb::CachedSchedule* last_cs = nullptr;  // schedule of the most recent launch
     nb::RankBuffers last_rb;
     cudaStream_t bench_stream = nullptr;
+    // host -> device updates of the comm's own state (view, window table,
+    // flags at init): an internal non-blocking stream, synchronized before the
+    // call returns -- the legacy stream would not order them before a peer
+    // rank's kernels on other streams (ranks sharing a device)
+    cudaStream_t aux = nullptr;
     uint64_t* d_trace = nullptr;  // NIMBLE_TRACE=1: device timeline of the last launch
     nb::DeviceStats* d_stats = nullptr;  // NIMBLE_STATS=1: per-kind byte counters, slot occupancy
     struct {
@@ -335,6 +341,17 @@ struct Clique {
 
 uint64_t ring_count(const nimbleComm* c, const nimbleCommConfig& cfg);
 
+// Complete host -> device writes of comm state (see nimbleComm::aux).
+void h2d(nimbleComm* c, void* dst, const void* src, size_t n) {
+    CUDA_TRY(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, c->aux));
+    CUDA_TRY(cudaStreamSynchronize(c->aux));
+}
+
+void zero(nimbleComm* c, void* dst, size_t n) {
+    CUDA_TRY(cudaMemsetAsync(dst, 0, n, c->aux));
+    CUDA_TRY(cudaStreamSynchronize(c->aux));
+}
+
 void upload_view(nimbleComm* c) {
     c->view.rank = c->rank;
     c->view.nranks = c->nranks;
@@ -351,7 +368,7 @@ void upload_view(nimbleComm* c) {
     c->view.epoch = c->d_epoch;
     const char* t = std::getenv("NIMBLE_TIMEOUT_MS");
     c->view.timeout_ms = t && *t ? static_cast<uint32_t>(std::atoi(t)) : 60000u;
-    CUDA_TRY(cudaMemcpy(c->d_view, &c->view, sizeof c->view, cudaMemcpyHostToDevice));
+    h2d(c, c->d_view, &c->view, sizeof c->view);
 }
 
 constexpr uint32_t kMaxWindows = 256;
@@ -437,7 +454,7 @@ void setup_regions(nimbleComm* c, bool single_process) {
     c->staging_bytes = staging_size(c);
     const uint64_t ctrl_bytes = FlagLayout::bytes(c->nranks);
     CUDA_TRY(cudaMalloc(&c->ctrl, ctrl_bytes));
-    CUDA_TRY(cudaMemset(c->ctrl, 0, ctrl_bytes));
+    zero(c, c->ctrl, ctrl_bytes);
     CUDA_TRY(cudaMalloc(&c->staging, std::max<uint64_t>(c->staging_bytes, 256)));
     c->peer_ctrl.assign(static_cast<size_t>(c->nranks), nullptr);
     c->peer_staging.assign(static_cast<size_t>(c->nranks), nullptr);
@@ -493,13 +510,14 @@ void setup_regions(nimbleComm* c, bool single_process) {
 void setup_common(nimbleComm* c) {
     DeviceGuard g(c->device);
     CUDA_TRY(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
     CUDA_TRY(cudaMalloc(&c->d_view, sizeof(CommDevice)));
     CUDA_TRY(cudaMalloc(&c->d_win_table, sizeof(uint64_t) * kMaxWindows * kMaxRanks));
-    CUDA_TRY(cudaMemset(c->d_win_table, 0, sizeof(uint64_t) * kMaxWindows * kMaxRanks));
+    zero(c, c->d_win_table, sizeof(uint64_t) * kMaxWindows * kMaxRanks);
     CUDA_TRY(cudaMalloc(&c->d_epoch, sizeof(uint64_t)));
-    CUDA_TRY(cudaMemset(c->d_epoch, 0, sizeof(uint64_t)));
+    zero(c, c->d_epoch, sizeof(uint64_t));
     CUDA_TRY(cudaMalloc(&c->d_scratch, sizeof(uint32_t) * (2 + 2 * kMaxRanks)));
-    CUDA_TRY(cudaMemset(c->d_scratch, 0, sizeof(uint32_t) * (2 + 2 * kMaxRanks)));
+    zero(c, c->d_scratch, sizeof(uint32_t) * (2 + 2 * kMaxRanks));
     CUDA_TRY(cudaHostAlloc(&c->h_status, 64, cudaHostAllocMapped | cudaHostAllocPortable));
     std::memset(c->h_status, 0, 64);
     CUDA_TRY(cudaHostGetDevicePointer(&c->d_status, c->h_status, 0));
@@ -509,7 +527,7 @@ void setup_common(nimbleComm* c) {
         CUDA_TRY(cudaMalloc(&c->d_trace, sizeof(uint64_t) * kTraceSlots));
     if (const char* t = std::getenv("NIMBLE_STATS"); t && *t == '1') {
         CUDA_TRY(cudaMalloc(&c->d_stats, sizeof(DeviceStats)));
-        CUDA_TRY(cudaMemset(c->d_stats, 0, sizeof(DeviceStats)));
+        zero(c, c->d_stats, sizeof(DeviceStats));
     }
     c->win_table.assign(static_cast<size_t>(kMaxWindows) * kMaxRanks, 0);
 }
@@ -1012,9 +1030,9 @@ void run_exchanges(std::vector<Exchange>& exs) {
         const int R = c->nranks;
         if (c->cfg.fabric != nimbleFabricAllToAll) continue;
         std::vector<uint64_t> m(static_cast<size_t>(R) * R, 0);
-        if (c->boot) {
+        if (c->boot) {  // host shared memory: the ranks share one machine (one NVLink box)
             std::vector<uint64_t> row(ex.rb.send_bytes);
-            c->boot->allgather(row.data(), row.size() * sizeof(uint64_t), m.data());
+            c->shm->allgather(row.data(), row.size() * sizeof(uint64_t), m.data(), c->view.timeout_ms);
         } else {
             for (Exchange& other : exs)
                 if (other.comm->clique == c->clique)
@@ -1130,17 +1148,15 @@ void* register_window(nimbleComm* c, void* buff, size_t size) {
             }
             c->win_table[static_cast<size_t>(id) * kMaxRanks + r] = addr;
         }
-        CUDA_TRY(cudaMemcpy(c->d_win_table + static_cast<size_t>(id) * kMaxRanks,
-                            &c->win_table[static_cast<size_t>(id) * kMaxRanks], sizeof(uint64_t) * kMaxRanks,
-                            cudaMemcpyHostToDevice));
+        h2d(c, c->d_win_table + static_cast<size_t>(id) * kMaxRanks, &c->win_table[static_cast<size_t>(id) * kMaxRanks],
+            sizeof(uint64_t) * kMaxRanks);
     } else {
         // single process: peers see each other's pointers directly; window k of
         // every comm in the clique is published as soon as it is registered
         for (nimbleComm* peer : c->clique->comms) {
             peer->win_table[static_cast<size_t>(id) * kMaxRanks + c->rank] = w.base;
             DeviceGuard pg(peer->device);
-            CUDA_TRY(cudaMemcpy(peer->d_win_table + static_cast<size_t>(id) * kMaxRanks + c->rank, &w.base,
-                                sizeof(uint64_t), cudaMemcpyHostToDevice));
+            h2d(peer, peer->d_win_table + static_cast<size_t>(id) * kMaxRanks + c->rank, &w.base, sizeof(uint64_t));
         }
     }
     c->windows.push_back(std::move(w));
@@ -1304,6 +1320,7 @@ nimbleResult_t nimbleCommInitRank(nimbleComm_t* out, int nranks, nimbleUniqueId 
         CUDA_TRY(cudaGetDevice(&c->device));
         nb::default_config(&c->cfg, nranks);
         c->boot = nb::bootstrap_connect(id, rank, nranks);
+        c->shm = std::make_unique<nb::ShmAllgather>(id, *c->boot);
         nb::setup_common(c.get());
         nb::setup_regions(c.get(), false);
         nb::upload_view(c.get());
@@ -1377,6 +1394,7 @@ nimbleComm::~nimbleComm() {
     if (d_stats) cudaFree(d_stats);
     if (h_status) cudaFreeHost(h_status);
     if (bench_stream) cudaStreamDestroy(bench_stream);
+    if (aux) cudaStreamDestroy(aux);
     if (last_launch) cudaEventDestroy(last_launch);
     cudaGetLastError();
     if (prev >= 0) cudaSetDevice(prev);
@@ -1489,7 +1507,7 @@ nimbleResult_t nimbleCommSetConfig(nimbleComm_t c, const nimbleCommConfig* cfg) 
             nb::free_regions(c);  // nulls the pointers: a failing setup below leaves nothing to double-free
             c->cfg = next;
             nb::setup_regions(c, false);
-            CUDA_TRY(cudaMemset(c->d_epoch, 0, sizeof(uint64_t)));  // fresh flags: epochs restart
+            nb::zero(c, c->d_epoch, sizeof(uint64_t));  // fresh flags: epochs restart
             nb::upload_view(c);
         }
         c->cfg = next;
@@ -1704,9 +1722,36 @@ nimbleResult_t nimbleCommGetStats(nimbleComm_t c, nimbleCommStats* out, int rese
         out->schedule_ns = c->host.schedule_ns;
         out->host_pad = 0;
         if (reset) {
-            CUDA_TRY(cudaMemset(c->d_stats, 0, sizeof(nb::DeviceStats)));
+            nb::zero(c, c->d_stats, sizeof(nb::DeviceStats));
             c->host = {};
         }
+    });
+}
+
+nimbleResult_t nimbleBootstrapShmAllgather(const nimbleUniqueId* id, int rank, int nranks, const void* in, size_t n,
+                                           void* out, int rounds) {
+    return guarded([&] {
+        if (!id || rounds < 1 || n + 8 > nb::ShmAllgather::kRecord || (n && (!in || !out)))
+            throw nb::Error(nimbleInvalidArgument, "bootstrap: bad argument");
+        auto b = nb::bootstrap_connect(*id, rank, nranks);
+        nb::ShmAllgather shm(*id, *b);
+        std::vector<uint8_t> rec(n + 8), all((n + 8) * static_cast<size_t>(nranks));
+        for (int k = 1; k <= rounds; ++k) {
+            const uint64_t tag = static_cast<uint64_t>(k) << 8 | static_cast<uint64_t>(rank);
+            std::memcpy(rec.data(), &tag, 8);
+            if (n) std::memcpy(rec.data() + 8, in, n);
+            shm.allgather(rec.data(), rec.size(), all.data(), 60000);
+            for (int r = 0; r < nranks; ++r) {  // every record is this round's, from its rank
+                uint64_t t = 0;
+                std::memcpy(&t, all.data() + static_cast<size_t>(r) * rec.size(), 8);
+                if (t != (static_cast<uint64_t>(k) << 8 | static_cast<uint64_t>(r)))
+                    throw nb::Error(nimbleInternalError, "shm allgather: stale or foreign record");
+            }
+        }
+        for (int r = 0; r < nranks; ++r)
+            if (n) std::memcpy(static_cast<uint8_t*>(out) + static_cast<size_t>(r) * n,
+                               all.data() + static_cast<size_t>(r) * rec.size() + 8, n);
+        b->barrier();  // nobody reads my record any more
     });
 }
 

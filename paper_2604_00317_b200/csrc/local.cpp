@@ -61,6 +61,8 @@ LocalCtx& context(int dev) {
     check(cudaMemset(v.status, 0, 64), "cudaMemset");
     check(cudaMalloc(&c.d_view, sizeof v), "cudaMalloc");
     check(cudaMemcpy(c.d_view, &v, sizeof v, cudaMemcpyHostToDevice), "cudaMemcpy");
+    // the setup above ran on the legacy stream; launches may come on any stream
+    check(cudaStreamSynchronize(cudaStreamLegacy), "cudaStreamSynchronize");
     c.ready = true;
     return c;
 }

@@ -29,6 +29,15 @@ def _worker(rank, world, port, q):
     mine = (ctypes.c_uint64 * 3)(rank, rank * 1000 + 7, 0xABCDEF)
     out = (ctypes.c_uint64 * (3 * world))()
     rc = _lib.lib().nimbleBootstrapAllgather(ctypes.byref(u), rank, world, mine, 24, out)
+    # the host shared-memory allgather (mesh-model rows), 2000 rounds back to back
+    uid2 = [C.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid2, 0)
+    u2 = _lib.UniqueId()
+    ctypes.memmove(ctypes.addressof(u2), uid2[0], 128)
+    out2 = (ctypes.c_uint64 * (3 * world))()
+    rc2 = _lib.lib().nimbleBootstrapShmAllgather(ctypes.byref(u2), rank, world, mine, 24, out2, 2000)
+    rc = rc or rc2
+    assert list(out2) == list(out) or rc2
     # bench.py helpers: per-rank matrix agreement and max-over-ranks timing
     import bench
     m = bench.workload_matrix(world, 1 << 20, 0.7)
