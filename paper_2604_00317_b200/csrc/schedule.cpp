@@ -2,6 +2,7 @@
 #include "schedule.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "capi_util.hpp"
@@ -126,6 +127,30 @@ void each_part(const std::vector<std::pair<uint64_t, uint64_t>>& parts, uint64_t
     }
 }
 
+// Experiment knobs (environment, read once; identical on every rank):
+//  NIMBLE_PUSH_SPAN = a in (0, 1]: direct pushes (and the self-ring drains
+//    that mirror them) take keys in [0, a): a port that pushes out while it
+//    pulls in finishes its stores -- and their acknowledgements, which its
+//    completion fence waits for -- before its pulls end;
+//  NIMBLE_PULL_TAIL = bytes: the last bytes of every pull flow are cut into
+//    NIMBLE_PULL_TAIL_CHUNK pieces, so the CTAs run out of work together.
+struct Knobs {
+    double push_span = 1.0;
+    uint64_t pull_tail = 0, pull_tail_chunk = 16 << 10;
+    Knobs() {
+        if (const char* e = std::getenv("NIMBLE_PUSH_SPAN"); e && *e) push_span = std::strtod(e, nullptr);
+        if (!(push_span > 0.0 && push_span <= 1.0)) push_span = 1.0;
+        if (const char* e = std::getenv("NIMBLE_PULL_TAIL"); e && *e) pull_tail = std::strtoull(e, nullptr, 0);
+        if (const char* e = std::getenv("NIMBLE_PULL_TAIL_CHUNK"); e && *e)
+            pull_tail_chunk = std::max<uint64_t>(4096, std::strtoull(e, nullptr, 0));
+    }
+};
+
+const Knobs& knobs() {
+    static const Knobs k;
+    return k;
+}
+
 // part keys span [off / total, (off + bytes) / total): the pair's progress
 double part_phase(uint64_t off, uint64_t total) { return static_cast<double>(off) / static_cast<double>(total); }
 double part_scale(uint64_t bytes, uint64_t total) { return static_cast<double>(bytes) / static_cast<double>(total); }
@@ -156,6 +181,7 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
     const uint64_t dchunk = std::min<uint64_t>(std::max<uint64_t>(direct_chunk, 4096), pipe_chunk);
     const uint64_t schunk = push_chunk ? std::min<uint64_t>(std::max<uint64_t>(push_chunk, 4096), pipe_chunk) : dchunk;
     Schedule sc;
+    const double span = knobs().push_span;
     sc.posts = rb.recv_post;
     sc.send_posts = rb.send_post;
     Cuts keyed;
@@ -224,8 +250,8 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
                     proto.peer = static_cast<uint8_t>(d);
                     each_part(rb.send_parts[d], schunk, [&](uint64_t ptr, uint64_t po, uint64_t pb, uint32_t seq0) {
                         proto.seq = seq0;
-                        sc.push_items[d] += cut(keyed, proto, ptr, po, pb, schunk, part_phase(po, pr.demand), false, 0,
-                                                part_scale(pb, pr.demand));
+                        sc.push_items[d] += cut(keyed, proto, ptr, po, pb, schunk, span * part_phase(po, pr.demand), false,
+                                                0, span * part_scale(pb, pr.demand));
                     });
                     sc.push_targets |= 1ull << d;
                     sc.write_targets |= 1ull << d;
@@ -234,7 +260,7 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
                     Item proto{};
                     proto.kind = kPush;
                     proto.peer = static_cast<uint8_t>(d);
-                    sc.push_items[d] += cut(keyed, proto, rb.send_ptr[d] + off, off, bytes, schunk, 0.0);
+                    sc.push_items[d] += cut(keyed, proto, rb.send_ptr[d] + off, off, bytes, schunk, 0.0, false, 0, span);
                     sc.push_targets |= 1ull << d;
                     sc.write_targets |= 1ull << d;
                     sc.moved_bytes += bytes;
@@ -250,8 +276,8 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
                     proto.aux = static_cast<uint16_t>(s);
                     each_part(rb.recv_parts[s], schunk, [&](uint64_t ptr, uint64_t po, uint64_t pb, uint32_t seq0) {
                         proto.seq = seq0;
-                        cut(keyed, proto, 0, ptr, pb, schunk, part_phase(po, pr.demand) + kHop2, false, 0,
-                            part_scale(pb, pr.demand));
+                        cut(keyed, proto, 0, ptr, pb, schunk, span * part_phase(po, pr.demand) + kHop2, false, 0,
+                            span * part_scale(pb, pr.demand));
                     });
                 } else if (d == me) {
                     sc.recv_direct |= 1ull << s;
@@ -261,8 +287,18 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
                         proto.kind = kPull;
                         proto.peer = static_cast<uint8_t>(s);
                         // source: offset inside the sender's segment
-                        sc.pull_items[s] += cut(keyed, proto, 0, rb.recv_ptr[s] + off, bytes, dchunk, 0.0, true,
-                                              rb.recv_ptr[s]);
+                        const uint64_t tail = knobs().pull_tail < bytes ? knobs().pull_tail : 0;
+                        if (tail) {  // body at dchunk, the last `tail` bytes finer (same progress keys overall)
+                            const uint64_t body = bytes - tail;
+                            sc.pull_items[s] += cut(keyed, proto, 0, rb.recv_ptr[s] + off, body, dchunk, 0.0, true,
+                                                  rb.recv_ptr[s], part_scale(body, bytes));
+                            sc.pull_items[s] += cut(keyed, proto, 0, rb.recv_ptr[s] + off + body, tail,
+                                                  knobs().pull_tail_chunk, part_phase(body, bytes), true, rb.recv_ptr[s],
+                                                  part_scale(tail, bytes));
+                        } else {
+                            sc.pull_items[s] += cut(keyed, proto, 0, rb.recv_ptr[s] + off, bytes, dchunk, 0.0, true,
+                                                  rb.recv_ptr[s]);
+                        }
                     }
                     if ((rb.recv_post[s].mode & 0xf) == kPostStaged) {  // drain my self ring (s, me)
                         Item proto{};
@@ -270,7 +306,7 @@ Schedule build_schedule(const PlanResult& plan, const RankBuffers& rb, uint64_t 
                         proto.peer = static_cast<uint8_t>(me);
                         proto.aux = static_cast<uint16_t>(s);
                         // chunk k of the ring is the sender's push item k: same cut
-                        cut(keyed, proto, 0, off, bytes, schunk, kHop2);
+                        cut(keyed, proto, 0, off, bytes, schunk, kHop2, false, 0, span);
                     } else {
                         sc.recv_zc |= 1ull << s;
                     }
