@@ -1455,6 +1455,11 @@ nimbleResult_t nimbleCommGetAsyncError(nimbleComm_t c, nimbleResult_t* err) {
                             (peer == 0xff ? std::string("?") : std::to_string(peer & 0x7f) +
                                                                    ((peer & 0x80) ? " [in]" : "")) +
                             ", epoch " + std::to_string(detail & 0xffff) + ")";
+        if (code == 9) {  // LL: what the polled line held
+            volatile uint32_t* st = reinterpret_cast<volatile uint32_t*>(c->h_status);
+            nb::g_last_error += " [line " + std::to_string(st[4]) + " of piece " + std::to_string(st[5]) +
+                                " held flags " + std::to_string(st[2]) + "/" + std::to_string(st[3]) + "]";
+        }
     }
     return nimbleSuccess;
 }

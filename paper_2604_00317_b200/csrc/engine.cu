@@ -569,7 +569,16 @@ __device__ void ll_recv_all(const LaunchArgs& a) {
                     if ((spin & 255) == 255) {
                         if (*status != 0) break;
                         if (global_ns() - t0 > limit) {
-                            latch(c, kErrLLTimeout, 0x80u | static_cast<uint32_t>(s), a.epoch);
+                            if (atomicCAS(c->status, 0u, static_cast<uint32_t>(kErrLLTimeout)) == 0u) {
+                                // what the line held: its two flag words, and which line / piece
+                                c->status[1] = (0x80u | static_cast<uint32_t>(s)) << 16 |
+                                               static_cast<uint32_t>(a.epoch & 0xffffu);
+                                c->status[2] = v.y;
+                                c->status[3] = v.w;
+                                c->status[4] = k;
+                                c->status[5] = it.seq;
+                                __threadfence_system();
+                            }
                             break;
                         }
                     }

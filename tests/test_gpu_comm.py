@@ -1069,3 +1069,39 @@ def test_moe_count_exchange_consistent(layout):
     for r in range(R):
         for s in range(R):
             assert out[r][1][s] == out[s][0][r], (r, s, out)
+
+
+def w_count_variants(comm, rank, R, variant, reps):
+    """Debug aid: the MoE count exchange (8-byte LL pairs + an 8-byte self
+    copy) `reps` times, with (variant) nothing else / torch kernels between
+    exchanges / five registered windows.  Returns the reps whose counts came
+    back wrong; raises on an async error."""
+    hs = []
+    if variant == "reg":
+        bufs = [torch.empty(1 << 20, dtype=torch.uint8, device="cuda") for _ in range(5)]
+        hs = [comm.register(b) for b in bufs]
+    out = torch.full((R,), rank + 1, dtype=torch.int64, device="cuda")
+    wrong = []
+    for i in range(reps):
+        if variant == "torch":
+            x = torch.rand(20000, device="cuda")
+            o = torch.argsort(x, stable=True)
+            torch.bincount(o % 7, minlength=R)
+        inn = torch.zeros(R, dtype=torch.int64, device="cuda")
+        out.fill_(rank + 1 + i)
+        comm.alltoall(out, inn, 8)
+        got = inn.tolist()
+        if got != [s + 1 + i for s in range(R)]:
+            wrong.append((i, got))
+    _sync()
+    comm.check_async()
+    for h in hs:
+        comm.deregister(h)
+    return wrong
+
+
+@pytest.mark.parametrize("variant", ["plain", "torch", "reg"])
+@pytest.mark.parametrize("layout", _layouts(4, proc=False))
+def test_count_exchange_variants(layout, variant):
+    out = _run(layout, "w_count_variants", variant, 30)
+    assert all(v == [] for v in out.values()), out
