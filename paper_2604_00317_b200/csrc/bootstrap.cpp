@@ -26,7 +26,15 @@ namespace nb {
 namespace {
 
 constexpr uint32_t kMagic = 0x4e4d4231;  // "NMB1"
-constexpr int kIoTimeoutMs = 600000;     // a silent peer for 10 min is dead
+// a silent peer for 10 min is dead (NIMBLE_BOOTSTRAP_TIMEOUT_MS overrides)
+int io_timeout_ms() {
+    static const int ms = [] {
+        const char* e = std::getenv("NIMBLE_BOOTSTRAP_TIMEOUT_MS");
+        const int v = e && *e ? std::atoi(e) : 0;
+        return v > 0 ? v : 600000;
+    }();
+    return ms;
+}
 
 struct IdBlob {
     uint32_t magic;
@@ -50,7 +58,7 @@ struct Hello {
 
 void wait_io(int fd, short ev) {
     pollfd p{fd, ev, 0};
-    int r = ::poll(&p, 1, kIoTimeoutMs);
+    int r = ::poll(&p, 1, io_timeout_ms());
     if (r == 0) throw Error(nimbleRemoteError, "bootstrap: peer timed out");
     if (r < 0 && errno != EINTR) sys_fail("poll");
 }

@@ -127,7 +127,9 @@ def _thread_server(R, conn):
     """Long-lived child process: runs worker calls as R threads on GPU 0."""
     # one hardware queue per stream: R ranks' streams must not alias onto one
     # queue (a spinning grid would block the peer grid queued behind it)
-    os.environ.update(NIMBLE_TIMEOUT_MS="15000", NIMBLE_STATS="1", CUDA_DEVICE_MAX_CONNECTIONS="32")
+    # (a rank that failed leaves the others in a host collective: fail fast)
+    os.environ.update(NIMBLE_TIMEOUT_MS="15000", NIMBLE_STATS="1", CUDA_DEVICE_MAX_CONNECTIONS="32",
+                      NIMBLE_BOOTSTRAP_TIMEOUT_MS="60000", NIMBLE_TRACE="1")
     torch.cuda.set_device(0)
     from paper_2604_00317_b200 import comm as C
     while True:
@@ -158,6 +160,8 @@ def _thread_server(R, conn):
                     err = ""
                     try:
                         err = f" [async error {comm.async_error()}]"
+                        t = comm.debug_trace()  # last launch: kernel start / done (globaltimer, one GPU)
+                        err += f" [last launch start {t[0] % 10**10} waited {t[6] % 10**10} ns]"
                     except Exception:
                         pass
                     out[rank] = "ERROR" + err + " " + traceback.format_exc()
@@ -1091,6 +1095,7 @@ def w_count_variants(comm, rank, R, variant, reps):
         out.fill_(rank + 1 + i)
         comm.alltoall(out, inn, 8)
         got = inn.tolist()
+        comm.check_async()  # fail at the first bad exchange (its trace is the last launch's)
         if got != [s + 1 + i for s in range(R)]:
             wrong.append((i, got))
     _sync()
