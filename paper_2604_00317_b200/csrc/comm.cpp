@@ -38,6 +38,7 @@
 namespace nb {
 cudaError_t launch_exchange(const LaunchArgs& args, int ctas, cudaStream_t stream, bool pdl = true);
 cudaError_t launch_gen(const GenArgs& g, cudaStream_t st);
+cudaError_t prepare_engine(int dev);
 cudaError_t launch_fill(void* buf, uint64_t first, uint64_t n, uint64_t seed, int s, int d, cudaStream_t st);
 cudaError_t launch_check(const void* buf, uint64_t first, uint64_t n, uint64_t seed, int s, int d, uint64_t* bad,
                          cudaStream_t st);
@@ -130,27 +131,24 @@ struct DevBuf {
         return *this;
     }
     ~DevBuf() { release(); }
-    // Stream-ordered (de)allocation: cudaFree would synchronize the whole
-    // device, and on a device hosting several ranks of one comm that means
-    // waiting for a peer's engine grid that may itself wait for this rank's
-    // next launch.  The buffer is idle whenever it grows or is released (the
-    // schedule cache waits for the entry's last launch first).
-    void assign(const std::vector<T>& v, cudaStream_t st) {
-        if (v.size() > n) {
-            if (p) CUDA_TRY(cudaFreeAsync(p, st));
-            p = nullptr;
-            CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(v.size(), 1) * sizeof(T), st));
-            n = v.size();
-        }
-        if (!v.empty()) CUDA_TRY(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
-    }
-    // room for at least m elements (contents undefined)
-    void reserve(size_t m, cudaStream_t st) {
+    // Stream-ordered (de)allocation from the comm's pool: cudaFree would
+    // synchronize the whole device, and on a device hosting several ranks of
+    // one comm that means waiting for a peer's engine grid that may itself
+    // wait for this rank's next launch.  The buffer is idle whenever it grows
+    // or is released (the schedule cache orders it after the entry's last
+    // launch first).  Capacity grows by powers of two.
+    void reserve(size_t m, cudaStream_t st, cudaMemPool_t pool) {
         if (m <= n && p) return;
         if (p) CUDA_TRY(cudaFreeAsync(p, st));
         p = nullptr;
-        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(m, 1) * sizeof(T), st));
-        n = std::max<size_t>(m, 1);
+        size_t cap = 64;
+        while (cap < m) cap *= 2;
+        CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), cap * sizeof(T), pool, st));
+        n = cap;
+    }
+    void assign(const std::vector<T>& v, cudaStream_t st, cudaMemPool_t pool) {
+        reserve(v.size(), st, pool);
+        if (!v.empty()) CUDA_TRY(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
     }
     void release() {
         if (p) cudaFreeAsync(p, cudaStreamPerThread);
@@ -300,6 +298,7 @@ struct nimbleComm {
     // call returns -- the legacy stream would not order them before a peer
     // rank's kernels on other streams (ranks sharing a device)
     cudaStream_t aux = nullptr;
+    cudaMemPool_t pool = nullptr;  // schedule buffers (DevBuf)
     uint64_t* d_trace = nullptr;  // NIMBLE_TRACE=1: device timeline of the last launch
     nb::DeviceStats* d_stats = nullptr;  // NIMBLE_STATS=1: per-kind byte counters, slot occupancy
     struct {
@@ -510,7 +509,25 @@ void setup_regions(nimbleComm* c, bool single_process) {
 void setup_common(nimbleComm* c) {
     DeviceGuard g(c->device);
     CUDA_TRY(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
+    CUDA_TRY(prepare_engine(c->device));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    // The comm's own memory pool for schedule buffers, which grow while
+    // other ranks' engines may be running: it keeps what it maps (release
+    // threshold: never) and starts with room for ~500k work items, so a new
+    // schedule normally allocates without touching the device's mappings.
+    {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = c->device;
+        CUDA_TRY(cudaMemPoolCreate(&c->pool, &props));
+        uint64_t keep = ~0ull;
+        CUDA_TRY(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        void* warm = nullptr;
+        CUDA_TRY(cudaMallocFromPoolAsync(&warm, 16ull << 20, c->pool, c->aux));
+        CUDA_TRY(cudaFreeAsync(warm, c->aux));
+        CUDA_TRY(cudaStreamSynchronize(c->aux));
+    }
     CUDA_TRY(cudaMalloc(&c->d_view, sizeof(CommDevice)));
     CUDA_TRY(cudaMalloc(&c->d_win_table, sizeof(uint64_t) * kMaxWindows * kMaxRanks));
     zero(c, c->d_win_table, sizeof(uint64_t) * kMaxWindows * kMaxRanks);
@@ -874,13 +891,13 @@ CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& 
         }
     }
     if (!cs.used) CUDA_TRY(cudaEventCreateWithFlags(&cs.used, cudaEventDisableTiming));
-    cs.finals.assign(cs.sc.final_waits, st);
+    cs.finals.assign(cs.sc.final_waits, st, c->pool);
     if (gen_on_device(cs.sc)) {
         // the flows travel as kernel parameters; the device merges them
-        cs.items.reserve(cs.sc.nitems, st);
-        cs.ll_items.reserve(cs.sc.n_ll_send + cs.sc.n_ll_recv, st);
-        cs.posts.reserve(static_cast<size_t>(rb.R), st);
-        cs.send_posts.reserve(static_cast<size_t>(rb.R), st);
+        cs.items.reserve(cs.sc.nitems, st, c->pool);
+        cs.ll_items.reserve(cs.sc.n_ll_send + cs.sc.n_ll_recv, st, c->pool);
+        cs.posts.reserve(static_cast<size_t>(rb.R), st, c->pool);
+        cs.send_posts.reserve(static_cast<size_t>(rb.R), st, c->pool);
         GenArgs g;
         fill_gen(g, cs.sc, rb.R);
         g.items = cs.items.p;
@@ -890,10 +907,10 @@ CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& 
         CUDA_TRY(launch_gen(g, st));
     } else {
         materialize(cs.sc);
-        cs.items.assign(cs.sc.items, st);
-        cs.posts.assign(cs.sc.posts, st);
-        cs.send_posts.assign(cs.sc.send_posts, st);
-        cs.ll_items.assign(cs.sc.ll_items, st);
+        cs.items.assign(cs.sc.items, st, c->pool);
+        cs.posts.assign(cs.sc.posts, st, c->pool);
+        cs.send_posts.assign(cs.sc.send_posts, st, c->pool);
+        cs.ll_items.assign(cs.sc.ll_items, st, c->pool);
     }
     c->schedules.push_front(std::move(cs));
     return c->schedules.front();
@@ -1395,6 +1412,7 @@ nimbleComm::~nimbleComm() {
     if (h_status) cudaFreeHost(h_status);
     if (bench_stream) cudaStreamDestroy(bench_stream);
     if (aux) cudaStreamDestroy(aux);
+    if (pool) cudaMemPoolDestroy(pool);  // released once its frees complete
     if (last_launch) cudaEventDestroy(last_launch);
     cudaGetLastError();
     if (prev >= 0) cudaSetDevice(prev);

@@ -48,6 +48,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 
 #include "device.cuh"
 
@@ -1064,16 +1065,26 @@ __global__ void check_kernel(const uint8_t* buf, uint64_t first, uint64_t n, uin
 
 // ---- host-side launchers (called from the comm runtime) ----
 
+cudaError_t prepare_engine(int dev) {
+    static std::mutex mu;
+    static bool done[64] = {};
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> g(mu);
+    if (done[dev]) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(exchange_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kEngineSmem));
+    if (e == cudaSuccess) done[dev] = true;
+    return e;
+}
+
 cudaError_t launch_exchange(const LaunchArgs& args, int ctas, cudaStream_t stream, bool pdl) {
-    static thread_local int configured_device = -1;
+    // Opt in to > 48 KB of dynamic shared memory, once per device for the
+    // process (prepare_engine, called at comm creation): changing a kernel's
+    // shared-memory configuration can serialize kernels of other streams, and
+    // a rank sharing the device may be spinning on a peer's flags right now.
     int dev = 0;
     cudaGetDevice(&dev);
-    if (configured_device != dev) {  // opt in to > 48 KB of dynamic shared memory (per device)
-        cudaError_t e = cudaFuncSetAttribute(exchange_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(kEngineSmem));
-        if (e != cudaSuccess) return e;
-        configured_device = dev;
-    }
+    if (cudaError_t e = prepare_engine(dev); e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(ctas));
     cfg.blockDim = dim3(kThreads);

@@ -147,6 +147,7 @@ def _thread_server(R, conn):
                 _CTX.mode, _CTX.barrier = "thread", barrier
                 s = torch.cuda.Stream()
                 with torch.cuda.stream(s):
+                    _warm_allocator(R)
                     comm = None
                     comm = C.Comm.init_rank(R, uid, rank)
                     out[rank] = globals()[fn](comm, rank, R, *args)
@@ -176,6 +177,19 @@ def _thread_server(R, conn):
 
 
 _SERVERS = {}
+
+
+def _warm_allocator(R):
+    """Fill this thread's stream with cached device memory before any
+    exchange (20 GiB per server, split over its ranks).  A cudaMalloc
+    issued while peer ranks' engines spin on this
+    rank's flags can keep this rank's next kernel from starting (device
+    memory allocation is one of CUDA's implicit synchronization points
+    between streams): the workers' tensors must come from the cache."""
+    big = torch.empty((20 << 30) // R, dtype=torch.uint8, device="cuda")
+    small = [torch.empty(256 << 10, dtype=torch.uint8, device="cuda") for _ in range(64)]
+    del big, small
+    torch.cuda.current_stream().synchronize()
 
 
 def _server(R):
