@@ -303,6 +303,7 @@ struct nimbleComm {
     nb::DeviceStats* d_stats = nullptr;  // NIMBLE_STATS=1: per-kind byte counters, slot occupancy
     struct {
         uint64_t calls = 0, ns = 0, ns_max = 0, plans = 0, plan_ns = 0, schedules = 0, schedule_ns = 0;
+        uint64_t launches = 0;
     } host;  // C ABI cost per data-path call (nimbleCommGetStats)
     cudaEvent_t last_launch = nullptr;  // launches on one comm are serialized across streams
     cudaStream_t last_stream = nullptr;
@@ -970,6 +971,14 @@ void pin_for_capture(CachedSchedule& cs, cudaStream_t st) {
     CUDA_TRY(cudaGraphRetainUserObject(graph, obj, 1, cudaGraphUserObjectMove));
 }
 
+bool launch_log() {
+    static const bool on = [] {
+        const char* e = std::getenv("NIMBLE_LAUNCH_LOG");
+        return e && *e == '1';
+    }();
+    return on;
+}
+
 void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream_t st) {
     LaunchArgs a{};
     a.items = cs.items.p;
@@ -1020,6 +1029,24 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     const bool eager = cap == cudaStreamCaptureStatusNone;
     if (eager && c->launched && st != c->last_stream) CUDA_TRY(cudaStreamWaitEvent(st, c->last_launch, 0));
     CUDA_TRY(launch_exchange(a, ctas, st, c->colocated <= 1));
+    if (launch_log()) {  // NIMBLE_LAUNCH_LOG=1: one stderr line per launch (debug aid)
+        std::string sb, rbs;
+        for (int r = 0; r < c->nranks; ++r) {
+            sb += (r ? "," : "") + std::to_string(rb.send_bytes[r]);
+            rbs += (r ? "," : "") + std::to_string(rb.recv_bytes[r]);
+        }
+        std::fprintf(stderr,
+                     "[nimble] t %llu rank %d launch %llu ctas %d items %u ll_send %u ll_recv %u ll_senders %llx "
+                     "pull_req %llx send [%s] recv [%s] stream %p%s\n",
+                     static_cast<unsigned long long>(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                                         std::chrono::system_clock::now().time_since_epoch())
+                                                         .count() %
+                                                     10000000000ll),
+                     c->rank, static_cast<unsigned long long>(++c->host.launches), ctas, a.nitems, a.n_ll_send,
+                     a.n_ll_recv, static_cast<unsigned long long>(a.ll_senders),
+                     static_cast<unsigned long long>(a.pull_req), sb.c_str(), rbs.c_str(), static_cast<void*>(st),
+                     eager ? "" : " (captured)");
+    }
     if (eager) {
         CUDA_TRY(cudaEventRecord(c->last_launch, st));
         CUDA_TRY(cudaEventRecord(cs.used, st));

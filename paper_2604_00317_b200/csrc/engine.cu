@@ -1073,6 +1073,14 @@ cudaError_t prepare_engine(int dev) {
     if (done[dev]) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(exchange_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kEngineSmem));
+    // Load every kernel of the library now (CUDA loads modules lazily, on a
+    // function's first launch, and a module load waits for the device's
+    // running kernels -- on a device hosting several ranks, peer engines that
+    // may be spinning on this rank's next launch).
+    cudaFuncAttributes fa;
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, gen_items_kernel);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, fill_kernel);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, check_kernel);
     if (e == cudaSuccess) done[dev] = true;
     return e;
 }

@@ -105,8 +105,10 @@ class MoEDispatcher:
         # counts first (one int64 per peer), then the rows
         self._enter(stream)
         self.comm.alltoall(self.count_out, self.count_in, 8, stream)
-        if stream is not None:
-            stream.synchronize()  # the counts are read on the host next
+        # the counts are read on the host next: wait with the GIL released
+        # (tolist() would block holding it -- a peer rank's thread in this
+        # process could then never launch the exchange this one waits for)
+        (stream if stream is not None else torch.cuda.current_stream()).synchronize()
         send_counts = self.count_out.tolist()
         recv_counts = self.count_in.tolist()
         if sum(recv_counts) > self.cap_recv:
@@ -207,6 +209,7 @@ def dispatch(comm: Comm, x: torch.Tensor, topk_ids: torch.Tensor, num_experts: i
     count_out = torch.bincount(dest, minlength=R)
     count_in = torch.empty_like(count_out)
     comm.alltoall(count_out, count_in, 8)
+    torch.cuda.current_stream().synchronize()  # GIL released while waiting (see MoEDispatcher.dispatch)
     sc, rc = count_out.tolist(), count_in.tolist()
     cid = comm_id(comm)
     recv_x = alltoallv_rows(x.index_select(0, order // k), sc, rc, cid)

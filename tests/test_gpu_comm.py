@@ -70,6 +70,15 @@ def _capture(fn):
     return g
 
 
+def _worker(fn):
+    """A worker of this module by name, or "module:function" (debug tools)."""
+    if ":" in fn:
+        import importlib
+        mod, name = fn.split(":")
+        return getattr(importlib.import_module(mod), name)
+    return globals()[fn]
+
+
 # ---------------------------------------------------------------- process mode
 
 def _free_port():
@@ -112,7 +121,7 @@ def _entry(fn, rank, world, port, q, args):
         uid = [C.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, 0)
         comm = C.Comm.init_rank(world, uid[0], rank)
-        res = globals()[fn](comm, rank, world, *args)
+        res = _worker(fn)(comm, rank, world, *args)
         dist.barrier()
         comm.destroy()
         dist.destroy_process_group()
@@ -128,8 +137,13 @@ def _thread_server(R, conn):
     # one hardware queue per stream: R ranks' streams must not alias onto one
     # queue (a spinning grid would block the peer grid queued behind it)
     # (a rank that failed leaves the others in a host collective: fail fast)
+    # Eager module loading: CUDA loads a kernel's module on its first launch,
+    # and a module load waits for the device's running kernels -- here, peer
+    # ranks' engines that may be spinning on this rank's next exchange (a
+    # torch kernel first used between two exchanges stalled them until their
+    # timeout).  The library loads its own kernels at comm creation.
     os.environ.update(NIMBLE_TIMEOUT_MS="15000", NIMBLE_STATS="1", CUDA_DEVICE_MAX_CONNECTIONS="32",
-                      NIMBLE_BOOTSTRAP_TIMEOUT_MS="60000", NIMBLE_TRACE="1")
+                      NIMBLE_BOOTSTRAP_TIMEOUT_MS="60000", NIMBLE_TRACE="1", CUDA_MODULE_LOADING="EAGER")
     torch.cuda.set_device(0)
     from paper_2604_00317_b200 import comm as C
     while True:
@@ -150,7 +164,7 @@ def _thread_server(R, conn):
                     _warm_allocator(R)
                     comm = None
                     comm = C.Comm.init_rank(R, uid, rank)
-                    out[rank] = globals()[fn](comm, rank, R, *args)
+                    out[rank] = _worker(fn)(comm, rank, R, *args)
                     s.synchronize()
                     barrier.wait(timeout=_CALL_TIMEOUT_S)
                     comm.destroy()
@@ -181,12 +195,12 @@ _SERVERS = {}
 
 def _warm_allocator(R):
     """Fill this thread's stream with cached device memory before any
-    exchange (20 GiB per server, split over its ranks).  A cudaMalloc
+    exchange (16 GiB per server, split over its ranks).  A cudaMalloc
     issued while peer ranks' engines spin on this
     rank's flags can keep this rank's next kernel from starting (device
     memory allocation is one of CUDA's implicit synchronization points
     between streams): the workers' tensors must come from the cache."""
-    big = torch.empty((20 << 30) // R, dtype=torch.uint8, device="cuda")
+    big = torch.empty((16 << 30) // R, dtype=torch.uint8, device="cuda")
     small = [torch.empty(256 << 10, dtype=torch.uint8, device="cuda") for _ in range(64)]
     del big, small
     torch.cuda.current_stream().synchronize()
@@ -194,6 +208,8 @@ def _warm_allocator(R):
 
 def _server(R):
     import multiprocessing as mp
+    for other in [r for r in _SERVERS if r != R]:  # one server (and its cached HBM) at a time
+        _stop(other)
     srv = _SERVERS.get(R)
     if srv is None or not srv[0].is_alive():
         ctx = mp.get_context("spawn")
@@ -210,19 +226,23 @@ def _kill(R):
     p.join(timeout=30)
 
 
+def _stop(R):
+    p, conn = _SERVERS.pop(R)
+    try:
+        conn.send(None)
+        p.join(timeout=30)
+    except Exception:
+        pass
+    if p.is_alive():
+        p.kill()
+        p.join(timeout=30)
+
+
 @pytest.fixture(scope="module", autouse=True)
 def _stop_servers():
     yield
     for R in list(_SERVERS):
-        p, conn = _SERVERS[R]
-        try:
-            conn.send(None)
-            p.join(timeout=30)
-        except Exception:
-            pass
-        if p.is_alive():
-            p.kill()
-        _SERVERS.pop(R, None)
+        _stop(R)
 
 
 def _threads(fn, R, *args):
@@ -287,6 +307,7 @@ def _host_check(rank, R, m, seed, recv):
     lib.orc_alltoallv(R, mat, (ctypes.c_void_p * R)(*[b.ctypes.data for b in sends]),
                       (ctypes.c_void_p * R)(*[w.ctypes.data for w in want]))
     n = sum(m[s * R + rank] for s in range(R))
+    _sync()
     got = recv[:n].cpu().numpy()
     return int((got != want[rank][:n]).sum())
 
@@ -1108,6 +1129,7 @@ def w_count_variants(comm, rank, R, variant, reps):
         inn = torch.zeros(R, dtype=torch.int64, device="cuda")
         out.fill_(rank + 1 + i)
         comm.alltoall(out, inn, 8)
+        _sync()  # GIL released while waiting: tolist() would block holding it
         got = inn.tolist()
         comm.check_async()  # fail at the first bad exchange (its trace is the last launch's)
         if got != [s + 1 + i for s in range(R)]:
