@@ -444,8 +444,24 @@ void enable_peer(int dev) {
 // the other ranks' grids spin.  So each grid takes SMs / 2k CTAs, and the
 // grids are launched without programmatic dependent launch (a grid whose
 // successor is pre-launched would hold twice its share).
+//
+// CUDA loads a kernel's module on the kernel's first launch (lazy loading,
+// the default), and a module load waits for the device's running kernels:
+// here, the peer ranks' grids, which spin until this rank's next exchange --
+// a kernel first used between two exchanges stalls every rank until the
+// engine's timeout (tools/first_use_probe.py).  The library loads its own
+// kernels at comm creation (prepare_engine); the process's other kernels
+// need CUDA_MODULE_LOADING=EAGER, said once on stderr.
 void set_share(nimbleComm* c) {
     c->sms_share = c->colocated <= 1 ? c->sms : std::max(1, c->sms / (2 * c->colocated));
+    static std::atomic<bool> warned{false};
+    const char* mode = std::getenv("CUDA_MODULE_LOADING");
+    if (c->colocated > 1 && !(mode && std::strcmp(mode, "EAGER") == 0) && !warned.exchange(true))
+        std::fprintf(stderr,
+                     "nimble: %d ranks of one comm share GPU %d and CUDA_MODULE_LOADING is not EAGER: a kernel "
+                     "loaded lazily between two exchanges waits for the peer ranks' running engines "
+                     "(set CUDA_MODULE_LOADING=EAGER before CUDA initializes)\n",
+                     c->colocated, c->device);
 }
 
 // Allocate ctrl + staging, exchange handles / pointers, map peers.

@@ -137,13 +137,8 @@ def _thread_server(R, conn):
     # one hardware queue per stream: R ranks' streams must not alias onto one
     # queue (a spinning grid would block the peer grid queued behind it)
     # (a rank that failed leaves the others in a host collective: fail fast)
-    # Eager module loading: CUDA loads a kernel's module on its first launch,
-    # and a module load waits for the device's running kernels -- here, peer
-    # ranks' engines that may be spinning on this rank's next exchange (a
-    # torch kernel first used between two exchanges stalled them until their
-    # timeout).  The library loads its own kernels at comm creation.
     os.environ.update(NIMBLE_TIMEOUT_MS="15000", NIMBLE_STATS="1", CUDA_DEVICE_MAX_CONNECTIONS="32",
-                      NIMBLE_BOOTSTRAP_TIMEOUT_MS="60000", NIMBLE_TRACE="1", CUDA_MODULE_LOADING="EAGER")
+                      NIMBLE_BOOTSTRAP_TIMEOUT_MS="60000", NIMBLE_TRACE="1")
     torch.cuda.set_device(0)
     from paper_2604_00317_b200 import comm as C
     while True:
@@ -215,7 +210,21 @@ def _server(R):
         ctx = mp.get_context("spawn")
         parent, child = ctx.Pipe()
         p = ctx.Process(target=_thread_server, args=(R, child), daemon=True)
-        p.start()
+        # Eager module loading in the server (set before its CUDA init, which
+        # importing this module already does): CUDA loads a kernel's module on
+        # its first launch, and a module load waits for the device's running
+        # kernels -- here peer ranks' engines spinning on this rank's next
+        # exchange, so a torch kernel first used between two exchanges stalled
+        # them until their timeout (tools/first_use_probe.py).
+        prev = os.environ.get("CUDA_MODULE_LOADING")
+        os.environ["CUDA_MODULE_LOADING"] = "EAGER"
+        try:
+            p.start()
+        finally:
+            if prev is None:
+                os.environ.pop("CUDA_MODULE_LOADING")
+            else:
+                os.environ["CUDA_MODULE_LOADING"] = prev
         srv = _SERVERS[R] = (p, parent)
     return srv
 
