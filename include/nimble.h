@@ -340,8 +340,10 @@ nimbleResult_t nimbleDebugScheduleDevice(nimblePlan_t plan, int rank, int ranks,
 /* Device timeline of the comm's last launch (%globaltimer ns): kernel start,
  * prologue done, first item, last item, CTAs done, completions signalled,
  * completions observed, first CTA done, latest work loops done, latest
- * completion fence, earliest work loops done (16 slots).  Needs NIMBLE_TRACE=1
- * at comm creation; n >= 16. */
+ * completion fence, earliest work loops done (16 slots); then, for CTA i < 160,
+ * 6 words at 16 + 6 i: first item, queue empty, loops done, fence done (ns),
+ * bytes stored into peers, bytes pulled or copied locally.  Needs
+ * NIMBLE_TRACE=1 at comm creation; n >= 16 (up to 976 words are written). */
 nimbleResult_t nimbleCommDebugTrace(nimbleComm_t comm, uint64_t* out, int n);
 
 /* Device counters of the forwarding engine, accumulated over the comm's

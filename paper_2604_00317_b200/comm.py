@@ -132,11 +132,19 @@ class Comm:
         if e:
             raise _lib.NimbleError(e, _lib.lib().nimbleGetLastError().decode())
 
-    def debug_trace(self):
-        """Device timeline (ns) of the last launch; needs NIMBLE_TRACE=1."""
-        out = (c_u64 * 16)()
-        _lib.call("nimbleCommDebugTrace", self._h, out, 16)
-        return list(out)
+    def debug_trace(self, per_cta=False):
+        """Device timeline (ns) of the last launch; needs NIMBLE_TRACE=1.
+        per_cta: also the per-CTA words (include/nimble.h), as a second list
+        of [first, queue_empty, loops_done, fence_done, remote_bytes,
+        other_bytes] rows for the CTAs that ran."""
+        n = 16 + 160 * 6 if per_cta else 16
+        out = (c_u64 * n)()
+        _lib.call("nimbleCommDebugTrace", self._h, out, n)
+        v = list(out)
+        if not per_cta:
+            return v
+        rows = [v[16 + 6 * i:22 + 6 * i] for i in range(160)]
+        return v[:16], [r for r in rows if r[2]]
 
     STAT_KINDS = ("local", "push", "stage", "forward", "pull", "ll_send", "ll_recv", "drain")
 

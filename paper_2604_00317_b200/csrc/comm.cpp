@@ -558,7 +558,7 @@ void setup_common(nimbleComm* c) {
     CUDA_TRY(cudaStreamCreateWithFlags(&c->bench_stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&c->last_launch, cudaEventDisableTiming));
     if (const char* t = std::getenv("NIMBLE_TRACE"); t && *t == '1')
-        CUDA_TRY(cudaMalloc(&c->d_trace, sizeof(uint64_t) * kTraceSlots));
+        CUDA_TRY(cudaMalloc(&c->d_trace, sizeof(uint64_t) * kTraceWords));
     if (const char* t = std::getenv("NIMBLE_STATS"); t && *t == '1') {
         CUDA_TRY(cudaMalloc(&c->d_stats, sizeof(DeviceStats)));
         zero(c, c->d_stats, sizeof(DeviceStats));
@@ -987,6 +987,16 @@ void pin_for_capture(CachedSchedule& cs, cudaStream_t st) {
     CUDA_TRY(cudaGraphRetainUserObject(graph, obj, 1, cudaGraphUserObjectMove));
 }
 
+// Programmatic dependent launch between consecutive exchanges (NIMBLE_PDL=0
+// turns it off: A/B measurements, profilers that replay launches).
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("NIMBLE_PDL");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
 bool launch_log() {
     static const bool on = [] {
         const char* e = std::getenv("NIMBLE_LAUNCH_LOG");
@@ -1028,6 +1038,7 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     if (c->d_trace) {
         static const uint64_t init[kTraceSlots] = {~0ull, 0, ~0ull, 0, 0, 0, 0, ~0ull, 0, 0, ~0ull, 0, 0, 0, 0, 0};
         CUDA_TRY(cudaMemcpyAsync(c->d_trace, init, sizeof init, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemsetAsync(c->d_trace + kTraceSlots, 0, sizeof(uint64_t) * (kTraceWords - kTraceSlots), st));
         a.trace = c->d_trace;
     }
     int ctas = c->cfg.ctas > 0 ? c->cfg.ctas : c->sms_share;
@@ -1044,7 +1055,7 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     CUDA_TRY(cudaStreamIsCapturing(st, &cap));
     const bool eager = cap == cudaStreamCaptureStatusNone;
     if (eager && c->launched && st != c->last_stream) CUDA_TRY(cudaStreamWaitEvent(st, c->last_launch, 0));
-    CUDA_TRY(launch_exchange(a, ctas, st, c->colocated <= 1));
+    CUDA_TRY(launch_exchange(a, ctas, st, c->colocated <= 1 && pdl_enabled()));
     if (launch_log()) {  // NIMBLE_LAUNCH_LOG=1: one stderr line per launch (debug aid)
         std::string sb, rbs;
         for (int r = 0; r < c->nranks; ++r) {
@@ -1767,7 +1778,8 @@ nimbleResult_t nimbleCommDebugTrace(nimbleComm_t c, uint64_t* out, int n) {
         if (!c->d_trace) throw nb::Error(nimbleInvalidUsage, "trace: set NIMBLE_TRACE=1 before creating the comm");
         nb::DeviceGuard g(c->device);
         nb::quiesce(c);
-        CUDA_TRY(cudaMemcpy(out, c->d_trace, sizeof(uint64_t) * nb::kTraceSlots, cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(out, c->d_trace, sizeof(uint64_t) * static_cast<size_t>(std::min(n, nb::kTraceWords)),
+                            cudaMemcpyDeviceToHost));
     });
 }
 

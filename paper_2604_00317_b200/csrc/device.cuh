@@ -265,5 +265,18 @@ enum TraceSlot : int {
     kTraceLoopsDoneMin = 10, // min over CTAs: loops finished
     kTraceSlots = 16,
 };
+// Per-CTA timeline after the kTraceSlots launch-wide slots (NIMBLE_TRACE=1):
+// CTA i owns kTraceSlots + i * kCtaTraceSlots + k.
+enum CtaTraceSlot : int {
+    kCtaFirstItem = 0,    // producer: first item prepared (ns)
+    kCtaQueueEmpty = 1,   // producer: out of items (ns)
+    kCtaLoopsDone = 2,    // producer / consumers / signal warp finished (ns)
+    kCtaFenceDone = 3,    // completion fence done (ns)
+    kCtaRemoteBytes = 4,  // bytes this CTA stored into peer memory (push / stage / forward)
+    kCtaOtherBytes = 5,   // bytes it pulled or copied locally
+    kCtaTraceSlots = 6,
+};
+constexpr int kMaxCtaTrace = 160;
+constexpr int kTraceWords = kTraceSlots + kMaxCtaTrace * kCtaTraceSlots;
 
 }  // namespace nb

@@ -607,6 +607,8 @@ __device__ void produce(SharedState& sh, uint8_t* stages, const LaunchArgs& a) {
         return j;
     };
     bool first = true;
+    uint64_t remote_bytes = 0, other_bytes = 0;
+    uint64_t* ctr = a.trace && blockIdx.x < kMaxCtaTrace ? a.trace + kTraceSlots + blockIdx.x * kCtaTraceSlots : nullptr;
     auto next_slot = [&](uint32_t& slot) {
         slot = cnt % kStages;
         if (cnt >= kStages) mbar_wait(&sh.empty[slot], ((cnt / kStages) - 1) & 1);
@@ -619,10 +621,12 @@ __device__ void produce(SharedState& sh, uint8_t* stages, const LaunchArgs& a) {
         StageDesc end{};
         bool coherent = false;
         if (prepare(sh, a, it, src, dst, end, coherent) != kGo) continue;
-        if (it.kind == kPush || it.kind == kStage || (it.kind == kForward && it.peer != a.comm->rank))
-            sh.remote_writes = 1;
+        const bool remote = it.kind == kPush || it.kind == kStage || (it.kind == kForward && it.peer != a.comm->rank);
+        if (remote) sh.remote_writes = 1;
+        if (ctr) (remote ? remote_bytes : other_bytes) += it.bytes;
         if (first) {
             trace_min(a, kTraceFirstItem);
+            if (ctr) ctr[kCtaFirstItem] = global_ns();
             first = false;
         }
         uint32_t sig = 0;
@@ -701,6 +705,11 @@ __device__ void produce(SharedState& sh, uint8_t* stages, const LaunchArgs& a) {
         }
     }
     trace_max(a, kTraceLastItem);
+    if (ctr) {
+        ctr[kCtaQueueEmpty] = global_ns();
+        ctr[kCtaRemoteBytes] = remote_bytes;
+        ctr[kCtaOtherBytes] = other_bytes;
+    }
     uint32_t slot;
     next_slot(slot);
     sh.desc[slot].flags = kTerminate;
@@ -858,6 +867,7 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
     if (tid == 0) {
         trace_max(a, kTraceLoopsDoneMax);
         trace_min(a, kTraceLoopsDoneMin);
+        if (a.trace && blockIdx.x < kMaxCtaTrace) a.trace[kTraceSlots + blockIdx.x * kCtaTraceSlots + kCtaLoopsDone] = global_ns();
     }
     if (a.n_ll_recv) ll_recv_all(a);
     if (tid == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // next exchange may start launching
@@ -882,6 +892,7 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
             else asm volatile("fence.acq_rel.gpu;" ::: "memory");
             trace_min(a, kTraceFirstCtaDone);
             trace_max(a, kTraceFenceDoneMax);
+            if (a.trace && blockIdx.x < kMaxCtaTrace) a.trace[kTraceSlots + blockIdx.x * kCtaTraceSlots + kCtaFenceDone] = global_ns();
         }
         __syncwarp();
         if (!a.local_only && tid < R) {

@@ -169,6 +169,8 @@ def main():
         comm.set_config(pull=int(os.environ["SWEEP_PULL"]))
     if os.environ.get("SWEEP_LL_MAX"):
         comm.set_config(ll_max=int(os.environ["SWEEP_LL_MAX"]))
+    if os.environ.get("SWEEP_PUSH_CHUNK"):
+        comm.set_config(push_chunk=int(os.environ["SWEEP_PUSH_CHUNK"]))
     for chunk in [int(v) for v in os.environ.get("SWEEP_CHUNKS", "0").split(",")]:
         comm.set_config(direct_chunk=chunk)
         sweep(comm, pg, rank, world, chunk)

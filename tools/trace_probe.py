@@ -13,6 +13,29 @@ MiB = 1 << 20
 NAMES = ["start", "prolog", "first", "last", "ctas", "signal", "waited", "cta0done", "loopsmax", "fencemax", "loopsmin"]
 
 
+def _pct(v, q):
+    v = sorted(v)
+    return v[min(len(v) - 1, int(q * (len(v) - 1) + 0.5))] if v else float("nan")
+
+
+def cta_summary(t0, ctas):
+    """Per-CTA timeline: quantiles (min / median / max, us from kernel
+    start) of queue-empty, loops-done and fence-done, and the fence's
+    duration for CTAs that stored into peers vs those that did not."""
+    us = lambda x: (x - t0) / 1e3  # noqa: E731
+    out = [f"{len(ctas)} CTAs ({sum(1 for c in ctas if c[4])} with peer stores)"]
+    for name, k in (("first", 0), ("qempty", 1), ("loops", 2), ("fence", 3)):
+        v = [us(c[k]) for c in ctas if c[k]]
+        out.append(f"{name} {_pct(v, 0):.1f}/{_pct(v, .5):.1f}/{_pct(v, 1):.1f}")
+    for tag, sel in (("remote", lambda c: c[4] > 0), ("local", lambda c: c[4] == 0)):
+        d = [(c[3] - c[2]) / 1e3 for c in ctas if sel(c) and c[3] and c[2]]
+        if d:
+            out.append(f"fence[{tag}] {_pct(d, 0):.1f}/{_pct(d, .5):.1f}/{_pct(d, 1):.1f}")
+    mb = [(c[4] + c[5]) / 2**20 for c in ctas]
+    out.append(f"MiB/CTA {_pct(mb, 0):.2f}/{_pct(mb, .5):.2f}/{_pct(mb, 1):.2f}")
+    return "  ".join(out)
+
+
 def main():
     os.environ["NIMBLE_TRACE"] = "1"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -35,21 +58,22 @@ def main():
             elif case == "irregular":  # c4: total bytes over the whole matrix
                 m = P.gen_irregular(R, kib * 1024, 0.5, 1)
             else:
-                m = P.gen_skewed_a2av(R, kib * 1024, 0.7, 0)
+                m = P.gen_skewed_a2av(R, kib * 1024, float(os.environ.get("TRACE_RATIO", "0.7")), 0)
             sc, sd, rc, rd = C.packed_displs(m, R, rank)
             send = torch.empty(max(sum(sc), 16), dtype=torch.uint8, device="cuda")
             recv = torch.empty(max(sum(rc), 16), dtype=torch.uint8, device="cuda")
             hs, hr = comm.register(send), comm.register(recv)
             for _ in range(5):
                 comm.alltoallv(send, sc, sd, recv, rc, rd)
-            tr = comm.debug_trace()
+            tr = comm.debug_trace(per_cta=True)
             allt = [None] * world
             dist.all_gather_object(allt, tr)
             if rank == 0:
                 print(f"pull={pull} {kib} KiB/rank (us from each rank's own kernel start; globaltimers differ across GPUs)")
-                for r, t in enumerate(allt):
+                for r, (t, ctas) in enumerate(allt):
                     print(f"  rank {r}: " + " ".join(f"{n}={(v - t[0]) / 1e3:6.1f}" for n, v in zip(NAMES, t[:11])),
                           flush=True)
+                    print("    " + cta_summary(t[0], ctas), flush=True)
             comm.deregister(hs)
             comm.deregister(hr)
     dist.barrier()
