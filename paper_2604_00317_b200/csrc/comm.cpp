@@ -37,6 +37,7 @@
 
 namespace nb {
 cudaError_t launch_exchange(const LaunchArgs& args, int ctas, cudaStream_t stream, bool pdl = true);
+extern std::atomic<uint64_t> g_launch_seq;
 cudaError_t launch_gen(const GenArgs& g, cudaStream_t st);
 cudaError_t prepare_engine(int dev);
 cudaError_t launch_fill(void* buf, uint64_t first, uint64_t n, uint64_t seed, int s, int d, cudaStream_t st);
@@ -308,6 +309,14 @@ struct nimbleComm {
     cudaEvent_t last_launch = nullptr;  // launches on one comm are serialized across streams
     cudaStream_t last_stream = nullptr;
     bool launched = false;
+    // Epoch chaining (LaunchArgs::prev_epoch): the host's count of this comm's
+    // launches -- exact until a launch is captured into a CUDA graph (replays
+    // advance the device epoch unseen) -- and the library launch counter and
+    // stream right after the previous exchange.
+    uint64_t host_epoch = 0;
+    bool epoch_known = true;
+    uint64_t chain_seq = ~0ull;
+    cudaStream_t chain_stream = nullptr;
     // Frees whatever device / host state exists, so a comm whose init failed
     // half-way releases what it had allocated (nimbleCommDestroy first makes
     // sure no peer still touches it).
@@ -557,8 +566,14 @@ void setup_common(nimbleComm* c) {
     CUDA_TRY(cudaHostGetDevicePointer(&c->d_status, c->h_status, 0));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->bench_stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&c->last_launch, cudaEventDisableTiming));
-    if (const char* t = std::getenv("NIMBLE_TRACE"); t && *t == '1')
-        CUDA_TRY(cudaMalloc(&c->d_trace, sizeof(uint64_t) * kTraceWords));
+    if (const char* t = std::getenv("NIMBLE_TRACE"); t && *t == '1') {
+        CUDA_TRY(cudaMalloc(&c->d_trace, sizeof(uint64_t) * kTraceRegionWords));
+        std::vector<uint64_t> init(kTraceRegionWords, 0);
+        for (int b = 0; b < 2; ++b)
+            for (int k = 0; k < kTraceSlots; ++k)
+                if (trace_is_min_slot(k)) init[static_cast<size_t>(b * kTraceWords + k)] = ~0ull;
+        h2d(c, c->d_trace, init.data(), init.size() * sizeof(uint64_t));
+    }
     if (const char* t = std::getenv("NIMBLE_STATS"); t && *t == '1') {
         CUDA_TRY(cudaMalloc(&c->d_stats, sizeof(DeviceStats)));
         zero(c, c->d_stats, sizeof(DeviceStats));
@@ -997,6 +1012,16 @@ bool pdl_enabled() {
     return on;
 }
 
+// NIMBLE_CHAIN=0: every exchange waits for its predecessor's completion
+// (griddepcontrol.wait) instead of chaining on its epoch (A/B measurements).
+bool chain_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("NIMBLE_CHAIN");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
 bool launch_log() {
     static const bool on = [] {
         const char* e = std::getenv("NIMBLE_LAUNCH_LOG");
@@ -1035,12 +1060,7 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     // bound; other ratios within +-0.005; profiles/r01_pull_depth_n4.jsonl).
     a.pull_depth = 3;
     a.local_only = 0;
-    if (c->d_trace) {
-        static const uint64_t init[kTraceSlots] = {~0ull, 0, ~0ull, 0, 0, 0, 0, ~0ull, 0, 0, ~0ull, 0, 0, 0, 0, 0};
-        CUDA_TRY(cudaMemcpyAsync(c->d_trace, init, sizeof init, cudaMemcpyHostToDevice, st));
-        CUDA_TRY(cudaMemsetAsync(c->d_trace + kTraceSlots, 0, sizeof(uint64_t) * (kTraceWords - kTraceSlots), st));
-        a.trace = c->d_trace;
-    }
+    a.trace = c->d_trace;  // the kernel picks the timeline by epoch parity and resets the next one
     int ctas = c->cfg.ctas > 0 ? c->cfg.ctas : c->sms_share;
     // small exchanges: no more CTAs than items (each CTA costs a fence at exit)
     const size_t work = static_cast<size_t>(cs.sc.nitems) + cs.sc.n_ll_send + cs.sc.n_ll_recv;
@@ -1055,7 +1075,20 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     CUDA_TRY(cudaStreamIsCapturing(st, &cap));
     const bool eager = cap == cudaStreamCaptureStatusNone;
     if (eager && c->launched && st != c->last_stream) CUDA_TRY(cudaStreamWaitEvent(st, c->last_launch, 0));
-    CUDA_TRY(launch_exchange(a, ctas, st, c->colocated <= 1 && pdl_enabled()));
+    const bool pdl = c->colocated <= 1 && pdl_enabled();
+    // chain on the previous exchange's epoch when it is this stream's
+    // previous library launch (see engine.cu, exchange_kernel)
+    const bool chain = eager && pdl && c->epoch_known && chain_enabled() && c->launched && st == c->chain_stream &&
+                       c->chain_seq == g_launch_seq.load(std::memory_order_relaxed);
+    a.prev_epoch = chain ? c->host_epoch : kEpochUnknown;
+    CUDA_TRY(launch_exchange(a, ctas, st, pdl));
+    if (eager) {
+        ++c->host_epoch;
+        c->chain_seq = g_launch_seq.load(std::memory_order_relaxed);
+        c->chain_stream = st;
+    } else {
+        c->epoch_known = false;  // replays advance the device epoch unseen
+    }
     if (launch_log()) {  // NIMBLE_LAUNCH_LOG=1: one stderr line per launch (debug aid)
         std::string sb, rbs;
         for (int r = 0; r < c->nranks; ++r) {
@@ -1585,6 +1618,7 @@ nimbleResult_t nimbleCommSetConfig(nimbleComm_t c, const nimbleCommConfig* cfg) 
             c->cfg = next;
             nb::setup_regions(c, false);
             nb::zero(c, c->d_epoch, sizeof(uint64_t));  // fresh flags: epochs restart
+            c->host_epoch = 0;
             nb::upload_view(c);
         }
         c->cfg = next;
@@ -1778,8 +1812,10 @@ nimbleResult_t nimbleCommDebugTrace(nimbleComm_t c, uint64_t* out, int n) {
         if (!c->d_trace) throw nb::Error(nimbleInvalidUsage, "trace: set NIMBLE_TRACE=1 before creating the comm");
         nb::DeviceGuard g(c->device);
         nb::quiesce(c);
-        CUDA_TRY(cudaMemcpy(out, c->d_trace, sizeof(uint64_t) * static_cast<size_t>(std::min(n, nb::kTraceWords)),
-                            cudaMemcpyDeviceToHost));
+        uint64_t epoch = 0;  // the latest launch's timeline: buffer epoch & 1
+        CUDA_TRY(cudaMemcpy(&epoch, c->d_epoch, sizeof epoch, cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(out, c->d_trace + (epoch & 1) * nb::kTraceWords,
+                            sizeof(uint64_t) * static_cast<size_t>(std::min(n, nb::kTraceWords)), cudaMemcpyDeviceToHost));
     });
 }
 

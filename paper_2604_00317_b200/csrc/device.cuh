@@ -222,6 +222,8 @@ struct GenArgs {
     CutDesc cuts[kMaxGenCuts];
 };
 
+constexpr uint64_t kEpochUnknown = ~0ull;
+
 // Per-launch arguments (passed by value as a __grid_constant__ kernel parameter).
 struct LaunchArgs {
     const Item* items;
@@ -248,6 +250,9 @@ struct LaunchArgs {
     uint32_t pull_depth;              // max stages in flight per CTA for a pull (kStages: no cap)
     uint32_t local_only;              // 1: flagless single-GPU exchange (no ctrl)
     uint64_t* trace;                  // optional globaltimer stamps (NIMBLE_TRACE=1), see kTrace*
+    uint64_t prev_epoch;              // epoch of the previous launch on this comm, when the host knows it
+                                      // (kEpochUnknown: after graph captures); the kernel then chains
+                                      // on the epoch word instead of griddepcontrol.wait (engine.cu)
 };
 
 // Device timeline of one launch (ns, %globaltimer): written when tracing is on.
@@ -263,6 +268,8 @@ enum TraceSlot : int {
     kTraceLoopsDoneMax = 8,  // max over CTAs: producer / consumers / signal warp finished
     kTraceFenceDoneMax = 9,  // max over CTAs: completion fence done
     kTraceLoopsDoneMin = 10, // min over CTAs: loops finished
+    kTraceEntryMin = 11,     // min over CTAs: entered the kernel, before griddepcontrol.wait (PDL)
+    kTracePrevEnd = 12,      // the previous launch's last CTA finished (its last timestamp)
     kTraceSlots = 16,
 };
 // Per-CTA timeline after the kTraceSlots launch-wide slots (NIMBLE_TRACE=1):
@@ -278,5 +285,13 @@ enum CtaTraceSlot : int {
 };
 constexpr int kMaxCtaTrace = 160;
 constexpr int kTraceWords = kTraceSlots + kMaxCtaTrace * kCtaTraceSlots;
+// The trace region holds two such timelines, used by epoch parity (launch e
+// writes buffer e & 1 and its last CTA resets buffer (e + 1) & 1 for the
+// next launch -- no host operation between launches), then one persistent
+// word: the end time of the latest launch.
+constexpr int kTraceRegionWords = 2 * kTraceWords + 1;
+__host__ __device__ constexpr bool trace_is_min_slot(int k) {
+    return k == 0 || k == 2 || k == 7 || k == 10 || k == 11;
+}
 
 }  // namespace nb

@@ -47,6 +47,7 @@
 // the receiver's previous-but-one launch; LL receives only for LL sends.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <mutex>
 
@@ -825,9 +826,41 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // prior grids complete, their writes visible
+    const uint64_t entry_ns = args.trace && tid == 0 ? global_ns() : 0;
+    // Chaining to the previous exchange of this comm.  When the host knows
+    // that launch's epoch, wait for its last CTA's release of the epoch word
+    // (written after it reset the shared scratch and trace state): this grid
+    // (a programmatic dependent) then starts ~5 us before the previous grid's
+    // completion would release griddepcontrol.wait.  Otherwise (launches
+    // replayed from CUDA graphs), wait for the previous grid's completion.
+    // The host allows this only when the previous launch of the library on
+    // this stream was this comm's previous exchange.  A CTA that finds that
+    // exchange still running (epoch word behind) knows it is the primary of
+    // this launch -- any other work on the stream would have had to wait for
+    // its completion -- and chains on the epoch word; one that finds it done
+    // does the ordinary griddepcontrol.wait (cheap then), so work a user
+    // enqueued in between is always waited for.
+    __shared__ uint32_t need_wait;
+    if (tid == 0) {
+        need_wait = 1;
+        if (!args.local_only && args.prev_epoch != kEpochUnknown) {
+            const uint64_t* ep = c->epoch;
+            if (ld_acquire(ep) < args.prev_epoch) {
+                need_wait = 0;
+                for (uint32_t spin = 0; ld_acquire(ep) < args.prev_epoch; ++spin)
+                    if (spin > 64) __nanosleep(64);
+            }
+        }
+    }
+    __syncthreads();
+    if (need_wait) asm volatile("griddepcontrol.wait;" ::: "memory");  // prior grids complete, their writes visible
     if (tid == 0) {
         a.epoch = a.local_only ? 0 : *reinterpret_cast<volatile uint64_t*>(c->epoch) + 1;
+        if (a.trace) {  // this launch's timeline: buffer epoch & 1 (see kTraceRegionWords)
+            a.trace = args.trace + (a.epoch & 1) * kTraceWords;
+            atomicMin(reinterpret_cast<unsigned long long*>(a.trace + kTraceEntryMin), entry_ns);
+            if (blockIdx.x == 0) a.trace[kTracePrevEnd] = args.trace[2 * kTraceWords];
+        }
         trace_min(a, kTraceKernelStart);
     }
     __syncthreads();
@@ -940,10 +973,26 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
         __syncwarp();
         if (lane == 0) {
             trace_max(a, kTraceWaited);
-            if (!a.local_only) *c->epoch = a.epoch;
             scratch[0] = 0;
-            __threadfence();
             scratch[1] = 0;
+        }
+    }
+    if (last_cta) {
+        if (a.trace) {  // reset the other timeline for the next launch, stamp this one's end
+            __syncthreads();
+            uint64_t* next = args.trace + ((a.epoch + 1) & 1) * kTraceWords;
+            for (int k = tid; k < kTraceWords; k += kThreads)
+                next[k] = k < kTraceSlots && trace_is_min_slot(k) ? ~0ull : 0;
+            __syncthreads();
+            if (tid == 0) args.trace[2 * kTraceWords] = global_ns();
+        }
+        // Last: publish the epoch.  The next exchange of this comm (possibly
+        // already resident, see the chaining above) starts when it sees it,
+        // so everything this launch shares with it -- scratch, trace -- is
+        // reset before this release.
+        if (tid == 0 && !a.local_only) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(c->epoch), "l"(a.epoch) : "memory");
         }
     }
 }
@@ -1076,6 +1125,11 @@ __global__ void check_kernel(const uint8_t* buf, uint64_t first, uint64_t n, uin
 
 // ---- host-side launchers (called from the comm runtime) ----
 
+// Library kernel launches in this process, any stream (comm.cpp: an
+// exchange chains on its predecessor's epoch only when nothing else of the
+// library was launched since, see LaunchArgs::prev_epoch).
+std::atomic<uint64_t> g_launch_seq{0};
+
 cudaError_t prepare_engine(int dev) {
     static std::mutex mu;
     static bool done[64] = {};
@@ -1097,6 +1151,7 @@ cudaError_t prepare_engine(int dev) {
 }
 
 cudaError_t launch_exchange(const LaunchArgs& args, int ctas, cudaStream_t stream, bool pdl) {
+    g_launch_seq.fetch_add(1, std::memory_order_relaxed);
     // Opt in to > 48 KB of dynamic shared memory, once per device for the
     // process (prepare_engine, called at comm creation): changing a kernel's
     // shared-memory configuration can serialize kernels of other streams, and
@@ -1118,6 +1173,7 @@ cudaError_t launch_exchange(const LaunchArgs& args, int ctas, cudaStream_t strea
 }
 
 cudaError_t launch_gen(const GenArgs& g, cudaStream_t st) {
+    g_launch_seq.fetch_add(1, std::memory_order_relaxed);
     const uint32_t total = g.nitems + g.nll;
     if (!total && !g.R) return cudaSuccess;
     uint32_t blocks = (total + 255) / 256;
@@ -1137,6 +1193,7 @@ uint64_t payload_key(uint64_t seed, int s, int d) {
 }
 
 cudaError_t launch_fill(void* buf, uint64_t first, uint64_t n, uint64_t seed, int s, int d, cudaStream_t st) {
+    g_launch_seq.fetch_add(1, std::memory_order_relaxed);
     if (!n) return cudaSuccess;
     fill_kernel<<<grid_for((n >> 3) + 2), 256, 0, st>>>(static_cast<uint8_t*>(buf), first, n, payload_key(seed, s, d));
     return cudaGetLastError();
@@ -1144,6 +1201,7 @@ cudaError_t launch_fill(void* buf, uint64_t first, uint64_t n, uint64_t seed, in
 
 cudaError_t launch_check(const void* buf, uint64_t first, uint64_t n, uint64_t seed, int s, int d, uint64_t* bad,
                          cudaStream_t st) {
+    g_launch_seq.fetch_add(1, std::memory_order_relaxed);
     if (!n) return cudaSuccess;
     check_kernel<<<grid_for((n >> 3) + 2), 256, 0, st>>>(static_cast<const uint8_t*>(buf), first, n,
                                                          payload_key(seed, s, d),

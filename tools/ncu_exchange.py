@@ -31,11 +31,16 @@ def main():
     ap.add_argument("--calls", type=int, default=8)
     ap.add_argument("--case", default="c3")
     args = ap.parse_args()
+    if os.environ.get("NCU_DUMP_AFTER_S"):  # where a rank hangs (stack dump to stderr)
+        import faulthandler
+        faulthandler.dump_traceback_later(int(os.environ["NCU_DUMP_AFTER_S"]), repeat=True)
     rank, R = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
     os.environ.setdefault("NIMBLE_BOOTSTRAP_TIMEOUT_MS", "600000")
-    path = os.path.join(ROOT, "gpurun_out", f".ncu_uid_{os.environ.get('MASTER_PORT', '0')}")
+    path = os.path.join(ROOT, "gpurun_out", f".ncu_uid_{os.environ.get('MASTER_PORT', '0')}_{os.environ.get('TORCHELASTIC_RUN_ID', '')}")
     if rank == 0:
+        if os.path.exists(path):
+            os.remove(path)
         uid = C.unique_id()
         with open(path + ".tmp", "wb") as f:
             f.write(uid)
@@ -55,9 +60,11 @@ def main():
     for d in range(R):
         C.fill_payload(send[sd[d]:], 0, sc[d], 1, rank, d)
     hs = [comm.register(recv), comm.register(send)]
-    for _ in range(args.calls):
+    for k in range(args.calls):
         comm.alltoallv(send, sc, sd, recv, rc, rd)
+        print(f"rank {rank}: call {k} enqueued", file=sys.stderr, flush=True)
     torch.cuda.synchronize()
+    print(f"rank {rank}: synchronized", file=sys.stderr, flush=True)
     comm.check_async()
     bad = torch.zeros(1, dtype=torch.int64, device="cuda")
     for s in range(R):

@@ -10,7 +10,8 @@ from paper_2604_00317_b200 import comm as C  # noqa: E402
 from paper_2604_00317_b200 import planner as P  # noqa: E402
 
 MiB = 1 << 20
-NAMES = ["start", "prolog", "first", "last", "ctas", "signal", "waited", "cta0done", "loopsmax", "fencemax", "loopsmin"]
+NAMES = ["start", "prolog", "first", "last", "ctas", "signal", "waited", "cta0done", "loopsmax", "fencemax", "loopsmin",
+         "entry", "prevend"]
 
 
 def _pct(v, q):
@@ -71,7 +72,7 @@ def main():
             if rank == 0:
                 print(f"pull={pull} {kib} KiB/rank (us from each rank's own kernel start; globaltimers differ across GPUs)")
                 for r, (t, ctas) in enumerate(allt):
-                    print(f"  rank {r}: " + " ".join(f"{n}={(v - t[0]) / 1e3:6.1f}" for n, v in zip(NAMES, t[:11])),
+                    print(f"  rank {r}: " + " ".join(f"{n}={(v - t[0]) / 1e3:6.1f}" for n, v in zip(NAMES, t[:13])),
                           flush=True)
                     print("    " + cta_summary(t[0], ctas), flush=True)
             comm.deregister(hs)
