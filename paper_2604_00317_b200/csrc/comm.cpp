@@ -1022,6 +1022,16 @@ bool chain_enabled() {
     return on;
 }
 
+// Pull stages in flight per CTA (NIMBLE_PULL_DEPTH=1..6 for experiments; 3).
+uint32_t pull_depth() {
+    static const uint32_t d = [] {
+        const char* e = std::getenv("NIMBLE_PULL_DEPTH");
+        const long v = e && *e ? std::strtol(e, nullptr, 10) : 3;
+        return static_cast<uint32_t>(v < 1 ? 1 : (v > 6 ? 6 : v));
+    }();
+    return d;
+}
+
 bool launch_log() {
     static const bool on = [] {
         const char* e = std::getenv("NIMBLE_LAUNCH_LOG");
@@ -1058,7 +1068,7 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     // Pulls keep at most 3 stages (96 KB) in flight per CTA: plenty for the
     // link, and a shorter drain (c3 at 4 GPUs, r = 0.5: 0.726 -> 0.773 of the
     // bound; other ratios within +-0.005; profiles/r01_pull_depth_n4.jsonl).
-    a.pull_depth = 3;
+    a.pull_depth = pull_depth();
     a.local_only = 0;
     a.trace = c->d_trace;  // the kernel picks the timeline by epoch parity and resets the next one
     int ctas = c->cfg.ctas > 0 ? c->cfg.ctas : c->sms_share;

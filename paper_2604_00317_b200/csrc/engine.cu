@@ -840,22 +840,50 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
     // its completion -- and chains on the epoch word; one that finds it done
     // does the ordinary griddepcontrol.wait (cheap then), so work a user
     // enqueued in between is always waited for.
-    __shared__ uint32_t need_wait;
+    __shared__ uint32_t need_wait, early;
     if (tid == 0) {
         need_wait = 1;
-        if (!args.local_only && args.prev_epoch != kEpochUnknown) {
-            const uint64_t* ep = c->epoch;
-            if (ld_acquire(ep) < args.prev_epoch) {
-                need_wait = 0;
-                for (uint32_t spin = 0; ld_acquire(ep) < args.prev_epoch; ++spin)
-                    if (spin > 64) __nanosleep(64);
-            }
+        early = 0;
+        if (!args.local_only && args.prev_epoch != kEpochUnknown &&
+            ld_acquire(c->epoch) < args.prev_epoch) {
+            need_wait = 0;
+            early = 1;
+            a.epoch = args.prev_epoch + 1;
         }
     }
     __syncthreads();
+    const int me = c->rank, R = c->nranks;
+    // Prologue: publish where each sender's segment lands in my buffer, and
+    // where my outgoing segments live.  A chained launch does it before the
+    // previous exchange has released the epoch: that exchange is this
+    // launch's primary (so no other work touched the buffers in between) and
+    // all its CTAs are past their data movement (they triggered this
+    // launch), so the posts for the next epoch can go out now -- peers start
+    // moving data into / out of my buffers ~a completion latency earlier.
+    auto publish_posts = [&]() {
+        if (a.local_only || blockIdx.x != 0 || tid >= 2 * R) return;
+        const bool send_side = tid >= R;
+        const int peer = send_side ? tid - R : tid;
+        const Post p = send_side ? a.send_posts[peer] : a.posts[peer];
+        if (!p.tag) return;
+        // pushed to the reader (it polls local memory); my own copy of a
+        // receive post serves relays
+        CtrlHeader* ph = reinterpret_cast<CtrlHeader*>(c->ctrl[peer]);
+        const int e = static_cast<int>(a.epoch & 1);
+        if (send_side) {
+            write_post(&ph->send_post[e][me], a.epoch, p);
+        } else {
+            write_post(&ph->post_in[e][me], a.epoch, p);
+            write_post(&reinterpret_cast<CtrlHeader*>(c->ctrl[me])->post[e][peer], a.epoch, p);
+        }
+    };
+    if (early) publish_posts();
+    if (tid == 0 && early)
+        for (uint32_t spin = 0; ld_acquire(c->epoch) < args.prev_epoch; ++spin)
+            if (spin > 64) __nanosleep(64);
     if (need_wait) asm volatile("griddepcontrol.wait;" ::: "memory");  // prior grids complete, their writes visible
     if (tid == 0) {
-        a.epoch = a.local_only ? 0 : *reinterpret_cast<volatile uint64_t*>(c->epoch) + 1;
+        if (!early) a.epoch = a.local_only ? 0 : *reinterpret_cast<volatile uint64_t*>(c->epoch) + 1;
         if (a.trace) {  // this launch's timeline: buffer epoch & 1 (see kTraceRegionWords)
             a.trace = args.trace + (a.epoch & 1) * kTraceWords;
             atomicMin(reinterpret_cast<unsigned long long*>(a.trace + kTraceEntryMin), entry_ns);
@@ -865,25 +893,7 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
     }
     __syncthreads();
     uint32_t* scratch = c->scratch;
-    const int me = c->rank, R = c->nranks;
-    // Prologue: publish where each sender's segment lands in my buffer.
-    if (!a.local_only && blockIdx.x == 0 && tid < 2 * R) {
-        const bool send_side = tid >= R;
-        const int peer = send_side ? tid - R : tid;
-        const Post p = send_side ? a.send_posts[peer] : a.posts[peer];
-        if (p.tag) {
-            // pushed to the reader (it polls local memory); my own copy of a
-            // receive post serves relays
-            CtrlHeader* ph = reinterpret_cast<CtrlHeader*>(c->ctrl[peer]);
-            const int e = static_cast<int>(a.epoch & 1);
-            if (send_side) {
-                write_post(&ph->send_post[e][me], a.epoch, p);
-            } else {
-                write_post(&ph->post_in[e][me], a.epoch, p);
-                write_post(&reinterpret_cast<CtrlHeader*>(c->ctrl[me])->post[e][peer], a.epoch, p);
-            }
-        }
-    }
+    if (!early) publish_posts();
     __syncthreads();
     if (tid == 0 && blockIdx.x == 0) trace_max(a, kTracePrologueDone);
     if (a.n_ll_send) ll_send_all(a);

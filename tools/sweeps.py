@@ -4,7 +4,9 @@ For the world size it is launched with (W), rank 0 prints one JSON line per
 point: nimble GB/s, fraction of the MCF port bound, NCCL all_to_all_single on
 the same buffers, relay flows, delivery mismatches.  Times: 5 warm-up + 100
 timed rounds (SWEEP_ITERS), per-round CUDA events, max over ranks per round;
-`us` is the median, `us_min` / `us_mean` beside it.
+`us` is the median, `us_min` / `us_mean` beside it; `us_block` times the same
+calls back to back between two events (bench.py's protocol, where
+consecutive exchanges chain without an event between them).
   c3  skewed all-to-allv, 256 MiB/rank, hotspot ratio 0.0 .. 0.9
   c5  uniform all-to-allv (ratio 1/(W-1)), 256 MiB/rank
   c4  irregular seeded matrix (seed 1, sparsity 0.5), total 1 KiB .. 1 GiB
@@ -96,6 +98,23 @@ def timed_graph(fn, st, iters, warmup):
     return max_over(e0.elapsed_time(e1) * 1e-3 / iters)
 
 
+def timed_block(fn, st, iters, warmup):
+    """`iters` back-to-back calls between two events (bench.py's protocol: no
+    event between calls, so consecutive exchanges chain), per-call mean, max
+    over ranks.  Returns seconds."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(iters):
+        fn()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return max_over(e0.elapsed_time(e1) * 1e-3 / iters)
+
+
 def _run_point(comm, pg, rank, R, m, name, fabric="nvswitch", iters=None, warmup=5, nccl=True, extra=None):
     iters = iters or int(os.environ.get("SWEEP_ITERS", "100"))
     comm.set_config(fabric=fabric, gpus_per_node=R)
@@ -109,6 +128,7 @@ def _run_point(comm, pg, rank, R, m, name, fabric="nvswitch", iters=None, warmup
     nvl0 = nvml_read()
     t, t_min, t_mean = timed(lambda: comm.alltoallv(send, sc, sd, recv, rc, rd, st), st, iters, warmup)
     nvl = nvml_delta(nvl0, nvml_read(), iters + warmup)
+    tb = timed_block(lambda: comm.alltoallv(send, sc, sd, recv, rc, rd, st), st, iters, warmup)
     comm.check_async()
     bad = torch.zeros(1, dtype=torch.int64, device="cuda")
     for s in range(R):
@@ -120,6 +140,7 @@ def _run_point(comm, pg, rank, R, m, name, fabric="nvswitch", iters=None, warmup
         out = torch.empty_like(recv)
         sv, rv = send[:sum(sc)], out[:sum(rc)]
         tn, _, _ = timed(lambda: dist.all_to_all_single(rv, sv, list(rc), list(sc), group=pg), st, iters, warmup)
+        tnb = timed_block(lambda: dist.all_to_all_single(rv, sv, list(rc), list(sc), group=pg), st, iters, warmup)
     graph = None
     if os.environ.get("SWEEP_GRAPH") == "1":  # host overhead removed, both arms
         st2 = torch.cuda.Stream()
@@ -141,7 +162,10 @@ def _run_point(comm, pg, rank, R, m, name, fabric="nvswitch", iters=None, warmup
            "us_min": t_min * 1e6, "us_mean": t_mean * 1e6, "iters": iters, "warmup": warmup,
            "gbps": total / t / 1e9, "bound_us": bound * 1e6, "frac_of_bound": bound / t if t else None,
            "nccl_us": tn * 1e6 if tn else None, "nccl_gbps": total / tn / 1e9 if tn else None,
-           "vs_nccl": (tn / t) if tn else None, "relay_flows": relays, "mismatched_bytes": mism}
+           "vs_nccl": (tn / t) if tn else None, "relay_flows": relays, "mismatched_bytes": mism,
+           # back-to-back calls between two events (bench.py's protocol)
+           "us_block": tb * 1e6, "frac_of_bound_block": bound / tb if tb else None,
+           "nccl_us_block": tnb * 1e6 if tn else None, "vs_nccl_block": (tnb / tb) if tn else None}
     if graph:
         row["graph"] = graph
     if nvl is not None:  # this rank's NVLink counters per call (rank 0 prints its own; hot rank = 0)
