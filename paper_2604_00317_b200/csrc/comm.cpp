@@ -559,8 +559,8 @@ void setup_common(nimbleComm* c) {
     zero(c, c->d_win_table, sizeof(uint64_t) * kMaxWindows * kMaxRanks);
     CUDA_TRY(cudaMalloc(&c->d_epoch, sizeof(uint64_t)));
     zero(c, c->d_epoch, sizeof(uint64_t));
-    CUDA_TRY(cudaMalloc(&c->d_scratch, sizeof(uint32_t) * (2 + 2 * kMaxRanks)));
-    zero(c, c->d_scratch, sizeof(uint32_t) * (2 + 2 * kMaxRanks));
+    CUDA_TRY(cudaMalloc(&c->d_scratch, sizeof(uint32_t) * kScratchWords));
+    zero(c, c->d_scratch, sizeof(uint32_t) * kScratchWords);
     CUDA_TRY(cudaHostAlloc(&c->h_status, 64, cudaHostAllocMapped | cudaHostAllocPortable));
     std::memset(c->h_status, 0, 64);
     CUDA_TRY(cudaHostGetDevicePointer(&c->d_status, c->h_status, 0));
@@ -820,6 +820,47 @@ void fill_posts(nimbleComm* c, RankBuffers& rb, const PlanResult& plan) {
 }
 
 constexpr size_t kCachedSchedules = 4;
+
+// NIMBLE_PUSH_LANE=0: no push lane (A/B measurements).
+bool push_lane_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("NIMBLE_PUSH_LANE");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
+// The push lane: a port that declines pulls (it sends plain posts: its
+// ingress dominates, profiles/r01_pull_policy.md) pushes its egress out while
+// it pulls its ingress in.  Mixed in one queue, every CTA ends with peer
+// stores in flight whose acknowledgements queue behind the saturated ingress,
+// and its completion fence waits for them (2.6-12.9 us per CTA at 64 MiB,
+// profiles/r02_trace_64_256mib_n4.txt).  With the pushes in their own queue,
+// taken first by a share of the CTAs proportional to their bytes, the pushes
+// finish early and the pulling CTAs end with a GPU-scope fence.  Direct
+// pushes only (nvswitch model: no relay rings).
+void set_push_lane(Schedule& sc, const RankBuffers& rb) {
+    uint64_t push = 0, other = 0;
+    bool declined = false;
+    for (const CutDesc& f : sc.cuts) {
+        if (f.proto.kind == kPush) {
+            push += f.bytes;
+            declined |= rb.send_post[f.proto.peer].mode == kSendPlain;
+        } else if (f.proto.kind == kPull) {
+            other += f.bytes;
+        } else if (f.proto.kind != kLocal && f.proto.kind != kForward) {
+            return;  // relay hops: one queue (the original ordering argument)
+        }
+    }
+    if (!declined || !push || !other) return;
+    for (CutDesc& f : sc.cuts)
+        if (f.proto.kind == kPush) {
+            f.flags |= kCutPushLane;
+            sc.n_push_lane += static_cast<uint32_t>(f.n);
+        }
+    sc.push_lane_bytes = push;
+    sc.main_bytes = other;
+}
 void reap_retired(nimbleComm* c);
 
 // Schedules whose flows fit the generator's parameter block are merged on
@@ -838,7 +879,7 @@ void fill_gen(GenArgs& g, const Schedule& sc, int R) {
     g.nitems = sc.nitems;
     g.nll = sc.n_ll_send + sc.n_ll_recv;
     g.R = static_cast<uint32_t>(R);
-    g.pad = 0;
+    g.n_push_lane = sc.n_push_lane;
     std::memset(g.post, 0, sizeof g.post);
     std::memset(g.send_post, 0, sizeof g.send_post);
     for (int r = 0; r < R && r < static_cast<int>(sc.posts.size()); ++r) g.post[r] = sc.posts[static_cast<size_t>(r)];
@@ -899,6 +940,7 @@ CachedSchedule& schedule_for(nimbleComm* c, uint64_t plan_id, const PlanResult& 
     const uint64_t dchunk = c->cfg.direct_chunk ? c->cfg.direct_chunk : kDefaultDirectChunk;
     cs.sc = build_schedule(plan, rb, c->cfg.pipe_chunk, slot_count(c->cfg), dchunk,
                            c->cfg.push_chunk ? c->cfg.push_chunk : kDefaultPushChunk, c->cfg.ll_max);
+    if (c->cfg.fabric == nimbleFabricNvSwitch && push_lane_enabled()) set_push_lane(cs.sc, rb);
     // Recycle the least recently used entry that no CUDA graph holds, once
     // kCachedSchedules of them exist: its buffers are rewritten on `st` after
     // its last launch (a stream wait on its event -- no host block, no
@@ -1044,6 +1086,7 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     LaunchArgs a{};
     a.items = cs.items.p;
     a.nitems = cs.sc.nitems;
+    a.n_push_lane = cs.sc.n_push_lane;
     a.slots = slot_count(c->cfg);
     a.pipe_chunk = c->cfg.pipe_chunk;
     a.epoch = 0;  // the kernel takes it from c->view.epoch (device), see engine.cu
@@ -1075,6 +1118,11 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     // small exchanges: no more CTAs than items (each CTA costs a fence at exit)
     const size_t work = static_cast<size_t>(cs.sc.nitems) + cs.sc.n_ll_send + cs.sc.n_ll_recv;
     ctas = std::max(1, std::min({ctas, c->sms, static_cast<int>(std::max<size_t>(work, 1))}));
+    if (cs.sc.n_push_lane) {  // CTAs for the push lane, by bytes (they join the main queue after)
+        const double share = static_cast<double>(cs.sc.push_lane_bytes) /
+                             static_cast<double>(cs.sc.push_lane_bytes + cs.sc.main_bytes);
+        a.push_ctas = static_cast<uint32_t>(std::clamp(static_cast<int>(share * ctas + 0.5), 1, std::max(1, ctas - 1)));
+    }
     // every rank launches even with nothing to move: its posts and done
     // flags are what its peers wait for.  Launches of one comm share its
     // scratch and flags, so a launch on another stream waits for the last one.

@@ -25,6 +25,10 @@
 namespace nb {
 
 constexpr int kMaxRanks = 32;
+// CommDevice::scratch words: [0] main queue head, [1] CTAs done, then the
+// per-peer grant decisions (2 x kMaxRanks), then the push-lane queue head.
+constexpr int kScratchPushHead = 2 + 2 * kMaxRanks;
+constexpr int kScratchWords = kScratchPushHead + 1;
 constexpr int kMaxSlots = 256;
 constexpr int kThreads = 512;  // forwarding-engine CTA size
 
@@ -69,7 +73,7 @@ static_assert(sizeof(Item) == 32, "Item layout");
 // flow, then to the earlier insertion index base + k.  The host merges the
 // flows into the item list (schedule.cpp, merge_cuts) or the device does
 // (engine.cu, gen_items_kernel) -- identical lists either way.
-enum CutFlags : uint32_t { kCutSrc = 1, kCutDst = 2, kCutPull = 4 };
+enum CutFlags : uint32_t { kCutSrc = 1, kCutDst = 2, kCutPull = 4, kCutPushLane = 8 };
 struct CutDesc {
     Item proto;             // kind / peer / aux / pad of every item of the flow
     uint64_t src0, dst0;    // item k: src = src0 + k * chunk (kCutSrc), dst = dst0 + k * chunk (kCutDst)
@@ -216,7 +220,8 @@ struct GenArgs {
     Post* posts;
     Post* send_posts;
     uint32_t ncuts, nkeyed, nitems, nll;
-    uint32_t R, pad;
+    uint32_t R;
+    uint32_t n_push_lane;  // items of the kCutPushLane flows: they come first in `items`
     Post post[kMaxRanks];
     Post send_post[kMaxRanks];
     CutDesc cuts[kMaxGenCuts];
@@ -250,6 +255,10 @@ struct LaunchArgs {
     uint32_t pull_depth;              // max stages in flight per CTA for a pull (kStages: no cap)
     uint32_t local_only;              // 1: flagless single-GPU exchange (no ctrl)
     uint64_t* trace;                  // optional globaltimer stamps (NIMBLE_TRACE=1), see kTrace*
+    uint32_t n_push_lane;             // items[0, n_push_lane): the push lane (direct pushes of a port that
+                                      // declined pulls), taken first by CTAs [0, push_ctas); the rest is
+                                      // the main queue, taken by every CTA
+    uint32_t push_ctas;
     uint64_t prev_epoch;              // epoch of the previous launch on this comm, when the host knows it
                                       // (kEpochUnknown: after graph captures); the kernel then chains
                                       // on the epoch word instead of griddepcontrol.wait (engine.cu)

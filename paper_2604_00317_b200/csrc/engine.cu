@@ -614,10 +614,22 @@ __device__ void produce(SharedState& sh, uint8_t* stages, const LaunchArgs& a) {
         slot = cnt % kStages;
         if (cnt >= kStages) mbar_wait(&sh.empty[slot], ((cnt / kStages) - 1) & 1);
     };
-    for (;;) {
-        const uint32_t index = atomicAdd(&scratch[0], 1u);
-        if (index >= a.nitems) break;
-        const Item it = a.items[index];
+    // The push lane first (CTAs [0, push_ctas)), then the main queue.  Each
+    // queue is in key order, so the deadlock-freedom argument holds per queue:
+    // a lane push waits only for posts and for its receiver's drain of slot
+    // k - S (the receiver's main queue), never for this rank's main queue.
+    const bool lane = blockIdx.x < a.push_ctas;
+    for (uint32_t* qhead = lane ? &scratch[kScratchPushHead] : &scratch[0];;) {
+        const bool main_q = qhead == &scratch[0];
+        const uint32_t qbase = main_q ? a.n_push_lane : 0;
+        const uint32_t qn = main_q ? a.nitems - a.n_push_lane : a.n_push_lane;
+        const uint32_t index = atomicAdd(qhead, 1u);
+        if (index >= qn) {
+            if (main_q) break;
+            qhead = &scratch[0];
+            continue;
+        }
+        const Item it = a.items[qbase + index];
         uint64_t src, dst;
         StageDesc end{};
         bool coherent = false;
@@ -985,6 +997,7 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
             trace_max(a, kTraceWaited);
             scratch[0] = 0;
             scratch[1] = 0;
+            scratch[kScratchPushHead] = 0;
         }
     }
     if (last_cta) {
@@ -1067,9 +1080,12 @@ __global__ void __launch_bounds__(256) gen_items_kernel(const __grid_constant__ 
             continue;
         }
         const double key = gen_key(f, k);
-        uint64_t pos = 0;
+        // position within the item's queue: the push lane first, then the rest
+        const uint32_t lane = f.flags & kCutPushLane;
+        uint64_t pos = lane ? 0 : g.n_push_lane;
         for (uint32_t h = 0; h < g.nkeyed; ++h) {
             const CutDesc& c = cuts[h];
+            if ((c.flags & kCutPushLane) != lane) continue;
             if (h == lo) {
                 pos += k;
                 continue;

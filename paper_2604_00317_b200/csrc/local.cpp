@@ -55,8 +55,8 @@ LocalCtx& context(int dev) {
     CommDevice v{};
     v.rank = 0;
     v.nranks = 1;
-    check(cudaMalloc(&v.scratch, sizeof(uint32_t) * (2 + 2 * kMaxRanks)), "cudaMalloc");
-    check(cudaMemset(v.scratch, 0, sizeof(uint32_t) * (2 + 2 * kMaxRanks)), "cudaMemset");
+    check(cudaMalloc(&v.scratch, sizeof(uint32_t) * kScratchWords), "cudaMalloc");
+    check(cudaMemset(v.scratch, 0, sizeof(uint32_t) * kScratchWords), "cudaMemset");
     check(cudaMalloc(&v.status, 64), "cudaMalloc");
     check(cudaMemset(v.status, 0, 64), "cudaMemset");
     check(cudaMalloc(&c.d_view, sizeof v), "cudaMalloc");

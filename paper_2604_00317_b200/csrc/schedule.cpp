@@ -100,6 +100,13 @@ std::vector<Item> merge_cuts(const std::vector<CutDesc>& flows) {
 
 void materialize(Schedule& sc) {
     sc.items = merge_cuts(sc.cuts);
+    if (sc.n_push_lane) {  // the push lane first, each queue in merge order (what the generator writes)
+        std::vector<CutDesc> lane, main;
+        for (const CutDesc& f : sc.cuts) ((f.flags & kCutPushLane) ? lane : main).push_back(f);
+        std::vector<Item> a = merge_cuts(lane), b = merge_cuts(main);
+        a.insert(a.end(), b.begin(), b.end());
+        sc.items = std::move(a);
+    }
     sc.ll_items.clear();
     for (const CutDesc& f : sc.ll_cuts)
         for (uint64_t k = 0; k < f.n; ++k) sc.ll_items.push_back(cut_item(f, k));

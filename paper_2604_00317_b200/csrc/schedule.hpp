@@ -38,6 +38,8 @@ struct Schedule {
     std::vector<CutDesc> cuts;     // the keyed flows (merged into the item list)
     std::vector<CutDesc> ll_cuts;  // LL sends, then LL receives (pieces enumerated in order)
     uint32_t nitems = 0;           // items of the keyed flows
+    uint32_t n_push_lane = 0;      // of which in the push lane (kCutPushLane flows; first in `items`)
+    uint64_t push_lane_bytes = 0, main_bytes = 0;
     std::vector<Item> items;       // materialize(): the merged list (host)
     std::vector<Item> ll_items;    // materialize(): LL sends, then LL receives (engine: LaunchArgs::ll_items)
     uint32_t n_ll_send = 0, n_ll_recv = 0;
