@@ -821,11 +821,13 @@ void fill_posts(nimbleComm* c, RankBuffers& rb, const PlanResult& plan) {
 
 constexpr size_t kCachedSchedules = 4;
 
-// NIMBLE_PUSH_LANE=0: no push lane (A/B measurements).
+// NIMBLE_PUSH_LANE=1: the push lane below (an experiment, off by default:
+// measured 0.78 -> 0.56 of the bound at c3 r = 0.7, 64 MiB, W=4; see
+// set_push_lane).
 bool push_lane_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("NIMBLE_PUSH_LANE");
-        return !(e && *e == '0');
+        return e && *e == '1';
     }();
     return on;
 }
@@ -839,6 +841,11 @@ bool push_lane_enabled() {
 // taken first by a share of the CTAs proportional to their bytes, the pushes
 // finish early and the pulling CTAs end with a GPU-scope fence.  Direct
 // pushes only (nvswitch model: no relay rings).
+// Measured (profiles/r02_push_lane_*): the lane's CTAs push at ~5 GB/s each
+// -- a port whose ingress is saturated gets its write acknowledgements late,
+// and each SM has only so many stores in flight -- so 48 CTAs need 270 us for
+// what all 148 CTAs, interleaving pushes with pulls, finish in 180 us.  Kept
+// as an opt-in experiment.
 void set_push_lane(Schedule& sc, const RankBuffers& rb) {
     uint64_t push = 0, other = 0;
     bool declined = false;
