@@ -140,6 +140,37 @@ def test_single_rank_comm_self_segment():
         c.destroy()
 
 
+def test_single_rank_chained_exchanges_see_user_kernels():
+    """Exchange chaining (engine.cu): back-to-back exchanges chain on the
+    epoch word, and an exchange whose predecessor on the stream is a user
+    kernel must still see that kernel's writes.  A 1-rank comm launches with
+    PDL, so both paths run here: every other step a torch kernel rewrites the
+    send buffer right before the exchange, and the result is checked on the
+    device after each step (no host sync in between)."""
+    from paper_2604_00317_b200 import comm as C
+    c = C.Comm.init_rank(1, C.unique_id(), 0)
+    try:
+        n = 5 * MiB + 3
+        x = torch.zeros(n, dtype=torch.uint8, device="cuda")
+        y = torch.zeros_like(x)
+        hx, hy = c.register(x), c.register(y)
+        c.alltoallv(x, [n], [0], y, [n], [0])  # warm-up: schedule cached
+        bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+        for k in range(60):
+            if k % 2 == 0:
+                x.fill_(k & 0xFF)  # a user kernel right before the exchange
+            c.alltoallv(x, [n], [0], y, [n], [0])
+            c.alltoallv(x, [n], [0], y, [n], [0])  # chained on the previous exchange
+            bad += (y != x).sum()
+        torch.cuda.synchronize()
+        c.check_async()
+        assert int(bad.item()) == 0
+        c.deregister(hx)
+        c.deregister(hy)
+    finally:
+        c.destroy()
+
+
 def test_comm_init_all_single_device():
     from paper_2604_00317_b200 import comm as C
     comms = C.Comm.init_all([0])
