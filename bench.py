@@ -538,7 +538,10 @@ def run_multi(args):
                      "frac": achieved / PORT_GBPS, "traffic": _ncu_traffic(f"n{R}"), "bound_ms": bound_s * 1e3,
                      "peak_source": "nominal NVLink-5 port, 900 GB/s per direction (north star); "
                                     "measured peer copy 770 GB/s (B200_PROFILING.md)",
-                     "algorithmic_bytes_per_launch": port, "kernel": "nb::exchange_kernel"},
+                     "algorithmic_bytes_per_launch": port, "kernel": "nb::exchange_kernel",
+                     "traffic_kind": "NVLink receive wire bytes (user + protocol) of the hot port per launch, "
+                                     "ncu nvlrx__bytes.sum (profiles/traffic.json); the bound is the port, "
+                                     "not DRAM"},
         "verified": {"mismatched_bytes": mismatches},
         "gpu_launches": args.steps * (2 if mats else 1),
         "clocks": clk.summary(),
