@@ -37,8 +37,9 @@
 // (proj/src/pipeline.cpp:97-106; device.cuh).  Every wait polls with acquire
 // loads and a global-timer timeout that latches an async error instead of
 // hanging the GPU.  Kernels are launched with programmatic stream
-// serialization: the next exchange's setup overlaps this one's tail and waits
-// (griddepcontrol.wait) before reading the launch epoch.
+// serialization: the next exchange's setup overlaps this one's tail, and it
+// either chains on this exchange's epoch release (when this exchange is its
+// programmatic primary) or waits for its completion (griddepcontrol.wait).
 //
 // Deadlock freedom: the scheduler sorts every rank's items by a global key
 // (chunk progress fraction), every wait targets an item with a strictly
@@ -815,8 +816,9 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
     // The launch's epoch comes from device memory, not the host: a launch
     // captured in a CUDA graph and replayed gets a fresh epoch every time.
     // Launched with programmatic stream serialization: this grid may start
-    // while the previous exchange on the stream is still finishing.  Everything
-    // up to griddepcontrol.wait touches only this CTA's shared memory.
+    // while the previous exchange on the stream is still finishing.  Until
+    // the chaining decision below, only this CTA's shared memory and the
+    // comm's immutable view are touched.
     __shared__ LaunchArgs a;
     if (threadIdx.x == 0) a = args;
     uint8_t* stages = reinterpret_cast<uint8_t*>(
