@@ -171,6 +171,33 @@ def test_single_rank_chained_exchanges_see_user_kernels():
         c.destroy()
 
 
+def test_two_comms_alternating_on_one_stream():
+    """Two comms' exchanges interleaved on one stream never chain on each
+    other (each launch's predecessor is the other comm's exchange, so it
+    waits for that grid): delivery stays exact and nothing hangs."""
+    from paper_2604_00317_b200 import comm as C
+    a = C.Comm.init_rank(1, C.unique_id(), 0)
+    b = C.Comm.init_rank(1, C.unique_id(), 0)
+    try:
+        n = 3 * MiB + 11
+        xa = torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda")
+        xb = torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda")
+        ya, yb = torch.zeros_like(xa), torch.zeros_like(xb)
+        bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+        for k in range(40):
+            a.alltoallv(xa, [n], [0], ya, [n], [0])
+            b.alltoallv(ya if k % 2 else xb, [n], [0], yb, [n], [0])  # b reads what a just wrote, half the time
+            bad += (ya != xa).sum() + (yb != (ya if k % 2 else xb)).sum()
+            xa.add_(1)
+        torch.cuda.synchronize()
+        a.check_async()
+        b.check_async()
+        assert int(bad.item()) == 0
+    finally:
+        a.destroy()
+        b.destroy()
+
+
 def test_comm_init_all_single_device():
     from paper_2604_00317_b200 import comm as C
     comms = C.Comm.init_all([0])
