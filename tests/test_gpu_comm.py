@@ -551,6 +551,30 @@ def w_graph(comm, rank, R):
     comm.check_async()
     comm.alltoallv(send, sc, sd, recv, rc, rd)  # eager launches keep working after replays
     _sync()
+    # The graph pins its schedule: more distinct exchanges than the schedule
+    # cache holds, then a deregistration (which drops every cached schedule),
+    # must leave the captured launch's buffers alive.
+    extra = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    hx = comm.register(extra)
+    for k in range(6):
+        mk = P.gen_skewed_a2av(R, MiB + 97 * k, 0.5, 0)
+        a, b, c_, d_ = C.packed_displs(mk, R, rank)
+        comm.alltoallv(send, a, b, recv, c_, d_)
+    _sync()
+    comm.deregister(hx)
+    _barrier()
+    for d in range(R):
+        C.fill_payload(send[sd[d]:], 0, sc[d], 300, rank, d)
+    recv.zero_()
+    _sync()
+    g.replay()
+    _sync()
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for s in range(R):
+        C.check_payload(recv[rd[s]:], 0, rc[s], 300, s, rank, bad)
+    _sync()
+    bads.append(int(bad.item()))
+    comm.check_async()
     comm.deregister(hs)
     comm.deregister(hr)
     return bads
@@ -936,7 +960,7 @@ def test_moe_dispatch_combine(layout):
 @pytest.mark.parametrize("layout", ALL)
 def test_cuda_graph_capture_and_replay(layout):
     for r, bads in _run(layout, "w_graph").items():
-        assert bads == [0] * 5, (r, bads)
+        assert bads == [0] * 6, (r, bads)  # 5 replays, then one after cache churn + a deregistration
 
 
 @pytest.mark.parametrize("layout", SOME)
