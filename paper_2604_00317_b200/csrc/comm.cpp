@@ -1081,6 +1081,16 @@ uint32_t pull_depth() {
     return d;
 }
 
+// NIMBLE_TAIL_ITEMS=n: the last n items of the queue pull one stage at a
+// time (experiment; 0 = off).
+uint32_t tail_items() {
+    static const uint32_t n = [] {
+        const char* e = std::getenv("NIMBLE_TAIL_ITEMS");
+        return static_cast<uint32_t>(e && *e ? std::strtoul(e, nullptr, 10) : 0);
+    }();
+    return n;
+}
+
 bool launch_log() {
     static const bool on = [] {
         const char* e = std::getenv("NIMBLE_LAUNCH_LOG");
@@ -1119,6 +1129,7 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     // link, and a shorter drain (c3 at 4 GPUs, r = 0.5: 0.726 -> 0.773 of the
     // bound; other ratios within +-0.005; profiles/r01_pull_depth_n4.jsonl).
     a.pull_depth = pull_depth();
+    a.tail_items = tail_items();
     a.local_only = 0;
     a.trace = c->d_trace;  // the kernel picks the timeline by epoch parity and resets the next one
     int ctas = c->cfg.ctas > 0 ? c->cfg.ctas : c->sms_share;

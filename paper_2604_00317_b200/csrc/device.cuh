@@ -253,6 +253,8 @@ struct LaunchArgs {
                                       // other end, seq = piece index, pad = the pair's byte count
     uint64_t ll_senders;              // senders whose LL slot I drain this launch
     uint32_t pull_depth;              // max stages in flight per CTA for a pull (kStages: no cap)
+    uint32_t tail_items;              // the last tail_items items of the main queue pull one stage at a
+                                      // time (a shorter ingress queue at the end: faster acknowledgements)
     uint32_t local_only;              // 1: flagless single-GPU exchange (no ctrl)
     uint64_t* trace;                  // optional globaltimer stamps (NIMBLE_TRACE=1), see kTrace*
     uint32_t n_push_lane;             // items[0, n_push_lane): the push lane (direct pushes of a port that

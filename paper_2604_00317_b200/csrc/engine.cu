@@ -680,8 +680,9 @@ __device__ void produce(SharedState& sh, uint8_t* stages, const LaunchArgs& a) {
             // (~16 KB per CTA covers the link's latency-bandwidth product): cap
             // a pull at pull_depth outstanding stages so the drain at the end
             // of the exchange stays short.
-            if (it.kind == kPull && a.pull_depth < kStages && cnt >= a.pull_depth) {
-                const uint32_t j = cnt - a.pull_depth;
+            const uint32_t depth = main_q && index + a.tail_items >= qn ? 1u : a.pull_depth;
+            if (it.kind == kPull && depth < kStages && cnt >= depth) {
+                const uint32_t j = cnt - depth;
                 mbar_wait(&sh.empty[j % kStages], (j / kStages) & 1);
             }
             StageDesc& ds = sh.desc[slot];

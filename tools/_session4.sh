@@ -1,12 +1,12 @@
-# round-2 4-GPU session: MoE caller vs NCCL with the round-2 engine; c5 push vs pull (block timing) (development aid)
+# round-2 4-GPU session: tail pull depth A/B (development aid)
 mkdir -p gpurun_out
-O=gpurun_out/s4i
+O=gpurun_out/s4j
 TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
-for T in 512 4096; do
-  MOE_T=$T timeout 600 $TR --nproc-per-node 4 --master-port 2970$((T % 7)) tools/moe_bench.py > ${O}_moe_T$T.jsonl 2> ${O}_moe_T$T.err
-  echo "moe T=$T: $(grep -c '^{' ${O}_moe_T$T.jsonl) rows"
+for ti in 0 148 296 592; do
+  NIMBLE_TAIL_ITEMS=$ti SWEEP_NCCL=0 SWEEP_PER_RANK_MIB=64 SWEEP_CASES=c3,c5 timeout 400 $TR --nproc-per-node 4 --master-port 29720 tools/sweeps.py > ${O}_tail${ti}_64.jsonl 2> ${O}_tail${ti}_64.err
 done
-for pl in 0 1; do
-  SWEEP_PULL=$pl SWEEP_PUSH_CHUNK=$([ $pl = 1 ] && echo 32768 || echo 0) SWEEP_CASES=c5 timeout 400 $TR --nproc-per-node 4 --master-port 2971$pl tools/sweeps.py > ${O}_c5_pull$pl.jsonl 2> ${O}_c5_pull$pl.err
+for ti in 0 296; do
+  NIMBLE_TAIL_ITEMS=$ti SWEEP_NCCL=0 SWEEP_PER_RANK_MIB=256 SWEEP_CASES=c3 timeout 400 $TR --nproc-per-node 4 --master-port 29721 tools/sweeps.py > ${O}_tail${ti}_256.jsonl 2> ${O}_tail${ti}_256.err
 done
+NIMBLE_TAIL_ITEMS=296 TRACE_PULL=0 TRACE_KIB=65536 timeout 300 $TR --nproc-per-node 4 --master-port 29722 tools/trace_probe.py > ${O}_trace296.txt 2>&1
 echo done
