@@ -1091,6 +1091,16 @@ uint32_t tail_items() {
     return n;
 }
 
+// NIMBLE_SPLIT_SIGNAL=0: the last CTA's warp 0 issues the completions owed to
+// peers before its own waits (A/B; default: warp 1 issues them in parallel).
+bool split_signal() {
+    static const bool on = [] {
+        const char* e = std::getenv("NIMBLE_SPLIT_SIGNAL");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
 bool launch_log() {
     static const bool on = [] {
         const char* e = std::getenv("NIMBLE_LAUNCH_LOG");
@@ -1130,6 +1140,7 @@ void launch(nimbleComm* c, CachedSchedule& cs, const RankBuffers& rb, cudaStream
     // bound; other ratios within +-0.005; profiles/r01_pull_depth_n4.jsonl).
     a.pull_depth = pull_depth();
     a.tail_items = tail_items();
+    a.split_signal = split_signal() ? 1u : 0u;
     a.local_only = 0;
     a.trace = c->d_trace;  // the kernel picks the timeline by epoch parity and resets the next one
     int ctas = c->cfg.ctas > 0 ? c->cfg.ctas : c->sms_share;

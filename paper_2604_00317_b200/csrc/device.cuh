@@ -253,6 +253,8 @@ struct LaunchArgs {
                                       // other end, seq = piece index, pad = the pair's byte count
     uint64_t ll_senders;              // senders whose LL slot I drain this launch
     uint32_t pull_depth;              // max stages in flight per CTA for a pull (kStages: no cap)
+    uint32_t split_signal;            // 1: the last CTA's warp 1 issues the completions owed to peers
+                                      // while warp 0 waits and releases the epoch (engine.cu)
     uint32_t tail_items;              // the last tail_items items of the main queue pull one stage at a
                                       // time (a shorter ingress queue at the end: faster acknowledgements)
     uint32_t local_only;              // 1: flagless single-GPU exchange (no ctrl)

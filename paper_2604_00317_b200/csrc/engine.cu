@@ -962,22 +962,34 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(const __grid_cons
         if (tid == 0) last_cta = atomicAdd(&scratch[1], 1u) + 1 == gridDim.x;
     }
     __syncthreads();
+    // The completions this launch owes its peers: done / pulled counters
+    // topped up to exactly 2^32 per peer, and the LL acknowledgement (this
+    // launch's LL slots are drained: acknowledged to every peer, LL sender now
+    // or not, so a sender's wait for epoch - 2 never depends on which pairs
+    // were small back then).  Issued by warp 1 while warp 0 waits for the
+    // peers' completions and releases the epoch: warp 0's release fence then
+    // does not wait for these remote writes' acknowledgements (which queue
+    // behind a saturated ingress), and nothing warp 0 waits for depends on
+    // them being issued first by warp 0 (NIMBLE_SPLIT_SIGNAL=0: warp 0 issues
+    // them itself, before its waits).
+    auto signal_peers = [&](int lane) {
+        const uint64_t full = 1ull << 32;
+        if (lane < R) {
+            CtrlHeader* ph = reinterpret_cast<CtrlHeader*>(c->ctrl[lane]);
+            red_add_sys(&ph->done[me], ((a.write_targets >> lane) & 1) ? full - gridDim.x : full);
+            red_add_sys(&ph->pulled[me], ((a.pull_req >> lane) & 1) ? full - gridDim.x : full);
+            st_relaxed(&ph->ll_ack[me], a.epoch);
+        }
+        __syncwarp();
+        if (lane == 0) trace_max(a, kTraceSignalled);
+    };
+    if (last_cta && a.split_signal && !a.local_only && tid >= 32 && tid < 64) signal_peers(tid - 32);
     if (last_cta && tid < 32) {
         const int lane = tid;
         if (lane == 0) trace_max(a, kTraceCtasDone);
         if (!a.local_only) {
-            const uint64_t full = 1ull << 32, done_tag = a.epoch << 32;
-            if (lane < R) {
-                CtrlHeader* ph = reinterpret_cast<CtrlHeader*>(c->ctrl[lane]);
-                red_add_sys(&ph->done[me], ((a.write_targets >> lane) & 1) ? full - gridDim.x : full);
-                red_add_sys(&ph->pulled[me], ((a.pull_req >> lane) & 1) ? full - gridDim.x : full);
-                // this launch's LL slots are drained: acknowledged to every peer,
-                // LL sender now or not, so a sender's wait for epoch - 2 never
-                // depends on which pairs were small back then
-                st_relaxed(&ph->ll_ack[me], a.epoch);
-            }
-            __syncwarp();
-            if (lane == 0) trace_max(a, kTraceSignalled);
+            const uint64_t done_tag = a.epoch << 32;
+            if (!a.split_signal) signal_peers(lane);
             for (uint32_t i = lane; i < a.nfinal; i += 32)  // relayed chunks drained from their rings
                 wait_ge(reinterpret_cast<const uint64_t*>(c->ctrl[me] + a.final_waits[2 * i]),
                         tag_of(a.epoch, static_cast<uint32_t>(a.final_waits[2 * i + 1])), c, kErrFinalTimeout);

@@ -1,12 +1,12 @@
-# round-2 4-GPU session: tail pull depth A/B (development aid)
+# round-2 4-GPU session: split peer signaling A/B + correctness (development aid)
 mkdir -p gpurun_out
-O=gpurun_out/s4j
+O=gpurun_out/s4k
 TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
-for ti in 0 148 296 592; do
-  NIMBLE_TAIL_ITEMS=$ti SWEEP_NCCL=0 SWEEP_PER_RANK_MIB=64 SWEEP_CASES=c3,c5 timeout 400 $TR --nproc-per-node 4 --master-port 29720 tools/sweeps.py > ${O}_tail${ti}_64.jsonl 2> ${O}_tail${ti}_64.err
+export CUDA_MODULE_LOADING=EAGER
+timeout 1200 python -m pytest tests/test_gpu_comm.py -k "proc or thread4" -q -p no:cacheprovider > ${O}_pytest.txt 2>&1
+echo "pytest: $(tail -1 ${O}_pytest.txt)"
+unset CUDA_MODULE_LOADING
+for sp in 1 0; do
+  NIMBLE_SPLIT_SIGNAL=$sp SWEEP_NCCL=0 SWEEP_PER_RANK_MIB=64 SWEEP_CASES=c3,c3k,c4 timeout 600 $TR --nproc-per-node 4 --master-port 2973$sp tools/sweeps.py > ${O}_split${sp}.jsonl 2> ${O}_split${sp}.err
 done
-for ti in 0 296; do
-  NIMBLE_TAIL_ITEMS=$ti SWEEP_NCCL=0 SWEEP_PER_RANK_MIB=256 SWEEP_CASES=c3 timeout 400 $TR --nproc-per-node 4 --master-port 29721 tools/sweeps.py > ${O}_tail${ti}_256.jsonl 2> ${O}_tail${ti}_256.err
-done
-NIMBLE_TAIL_ITEMS=296 TRACE_PULL=0 TRACE_KIB=65536 timeout 300 $TR --nproc-per-node 4 --master-port 29722 tools/trace_probe.py > ${O}_trace296.txt 2>&1
 echo done
