@@ -370,6 +370,57 @@ def w_skewed(comm, rank, R, per_rank, ratio, register):
     return _exchange_and_check(comm, rank, R, m, register, 11)
 
 
+def _ragged_matrix(R, seed):
+    """A seeded ragged matrix (identical on every rank): zero pairs, 1-byte
+    pairs, pairs around the LL piece (8 KiB) and the LL limit (1 MiB), and
+    multi-MiB pairs, with the self segment too."""
+    import random
+    rng = random.Random(seed)
+    sizes = [0, 0, 1, 7, 8191, 8193, (1 << 20) - 1, (1 << 20), (1 << 20) + 1, 3 * MiB + 5, 9 * MiB + 333]
+    return [rng.choice(sizes) for _ in range(R * R)]
+
+
+def w_ragged_fuzz(comm, rank, R, seeds):
+    """Ragged matrices at odd rank counts, each under three registration
+    layouts (receive windows registered everywhere / nowhere / on odd ranks
+    only -- staged and zero-copy receivers in one exchange), send windows
+    registered so receivers may pull: bit-exact on the device, rank 0 on the
+    host against orc_alltoallv, rings bounded."""
+    from paper_2604_00317_b200 import comm as C
+    out = []
+    for seed in seeds:
+        m = _ragged_matrix(R, seed)
+        for layout in ("all", "none", "odd"):
+            sc, sd, rc, rd = C.packed_displs(m, R, rank)
+            send = torch.empty(max(sum(sc), 16), dtype=torch.uint8, device="cuda")
+            recv = torch.full((max(sum(rc), 16),), 0xEE, dtype=torch.uint8, device="cuda")
+            scratch = torch.empty(4096, dtype=torch.uint8, device="cuda")
+            for d in range(R):
+                C.fill_payload(send[sd[d]:], 0, sc[d], seed, rank, d)
+            mine = layout == "all" or (layout == "odd" and rank % 2 == 1)
+            # registration is collective (one buffer per rank per call): the
+            # ranks that stay staged register a scratch buffer instead
+            hr = comm.register(recv if mine else scratch) if layout != "none" else None
+            hs = comm.register(send)
+            for _ in range(2):  # twice: the second call reuses the cached schedule (and chains)
+                comm.alltoallv(send, sc, sd, recv, rc, rd)
+            _sync()
+            comm.check_async()
+            bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+            for s_ in range(R):
+                C.check_payload(recv[rd[s_]:], 0, rc[s_], seed, s_, rank, bad)
+            _sync()
+            ok = int(bad.item()) == 0 and _rings_bounded(comm)
+            if rank == 0:
+                ok = ok and _host_check(rank, R, m, seed, recv) == 0
+            out.append(ok)
+            if hr is not None:
+                comm.deregister(hr)
+            comm.deregister(hs)
+            _barrier()
+    return out
+
+
 def w_pull_modes(comm, rank, R):
     """Receiver-driven pulls: every (pull mode, send registered, recv registered)
     combination delivers bit-exactly (granted pulls, declined pulls falling back
@@ -873,6 +924,12 @@ SOME = _layouts(2, 8)
 def test_skewed_alltoallv(layout, per_rank, ratio, register):
     for r, (bad, ok) in _run(layout, "w_skewed", per_rank, ratio, register).items():
         assert bad == 0 and ok, r
+
+
+@pytest.mark.parametrize("layout", _layouts(3, 5, 7, proc_min=3))
+def test_ragged_matrices_odd_rank_counts(layout):
+    for r, oks in _run(layout, "w_ragged_fuzz", [101, 202, 303]).items():
+        assert all(oks), (r, oks)
 
 
 @pytest.mark.parametrize("layout", ALL)
