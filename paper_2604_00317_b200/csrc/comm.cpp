@@ -115,6 +115,23 @@ struct DeviceGuard {
     }
 };
 
+// One internal stream per device for the library's own host -> device state
+// writes and stream-ordered frees, created once per process and never
+// destroyed.  A device offers a fixed number of hardware work queues (32
+// connections at most); every stream created maps onto one, round robin.  On
+// a device hosting several ranks of a comm, a stream that shares a queue
+// with a peer rank's spinning engine waits behind it -- so the library
+// creates no stream per comm (streams created and destroyed with every comm
+// keep shifting which queues collide).
+cudaStream_t internal_stream(int dev) {
+    static std::mutex mu;
+    static cudaStream_t streams[64] = {};
+    if (dev < 0 || dev >= 64) throw Error(nimbleInvalidArgument, "device index out of range");
+    std::lock_guard<std::mutex> g(mu);
+    if (!streams[dev]) CUDA_TRY(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
+    return streams[dev];
+}
+
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
@@ -152,7 +169,9 @@ struct DevBuf {
         if (!v.empty()) CUDA_TRY(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
     }
     void release() {
-        if (p) cudaFreeAsync(p, cudaStreamPerThread);
+        int dev = 0;
+        if (p && cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) cudaFreeAsync(p, internal_stream(dev));
+        else if (p) cudaFreeAsync(p, cudaStreamPerThread);
         p = nullptr;
         n = 0;
     }
@@ -536,7 +555,7 @@ void setup_common(nimbleComm* c) {
     DeviceGuard g(c->device);
     CUDA_TRY(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
     CUDA_TRY(prepare_engine(c->device));
-    CUDA_TRY(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    c->aux = internal_stream(c->device);
     // The comm's own memory pool for schedule buffers, which grow while
     // other ranks' engines may be running: it keeps what it maps (release
     // threshold: never) and starts with room for ~500k work items, so a new
@@ -564,7 +583,6 @@ void setup_common(nimbleComm* c) {
     CUDA_TRY(cudaHostAlloc(&c->h_status, 64, cudaHostAllocMapped | cudaHostAllocPortable));
     std::memset(c->h_status, 0, 64);
     CUDA_TRY(cudaHostGetDevicePointer(&c->d_status, c->h_status, 0));
-    CUDA_TRY(cudaStreamCreateWithFlags(&c->bench_stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&c->last_launch, cudaEventDisableTiming));
     if (const char* t = std::getenv("NIMBLE_TRACE"); t && *t == '1') {
         CUDA_TRY(cudaMalloc(&c->d_trace, sizeof(uint64_t) * kTraceRegionWords));
@@ -1385,7 +1403,7 @@ void bench_matrix(nimbleComm* c, const std::vector<uint64_t>& m, int warmup, int
         std::vector<void*> bufs;
         size_t first_window;
         ~Scope() {
-            cudaStreamSynchronize(c->bench_stream);
+            if (c->bench_stream) cudaStreamSynchronize(c->bench_stream);
             for (size_t k = first_window; k < c->windows.size(); ++k) {
                 c->windows[k].live = false;
                 for (void* p : c->windows[k].opened) ipc_cache().release(p);
@@ -1405,6 +1423,7 @@ void bench_matrix(nimbleComm* c, const std::vector<uint64_t>& m, int warmup, int
     auto* rbuf = static_cast<uint8_t*>(alloc(std::max<size_t>(rtot, 16)));
     auto* bad = static_cast<uint64_t*>(alloc(sizeof(uint64_t)));
     const uint64_t seed = 1;
+    if (!c->bench_stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->bench_stream, cudaStreamNonBlocking));
     cudaStream_t st = c->bench_stream;
     for (int p = 0; p < R; ++p) CUDA_TRY(launch_fill(sbuf + sd[p], 0, sc[p], seed, me, p, st));
     register_window(c, rbuf, std::max<size_t>(rtot, 16));
@@ -1584,8 +1603,7 @@ nimbleComm::~nimbleComm() {
     if (d_trace) cudaFree(d_trace);
     if (d_stats) cudaFree(d_stats);
     if (h_status) cudaFreeHost(h_status);
-    if (bench_stream) cudaStreamDestroy(bench_stream);
-    if (aux) cudaStreamDestroy(aux);
+    if (bench_stream) cudaStreamDestroy(bench_stream);  // created by the first bench entry point call
     if (pool) cudaMemPoolDestroy(pool);  // released once its frees complete
     if (last_launch) cudaEventDestroy(last_launch);
     cudaGetLastError();
