@@ -290,6 +290,8 @@ struct nimbleComm {
     std::vector<uint8_t*> peer_ctrl, peer_staging;
     std::vector<void*> ipc_mapped;  // ctrl / staging mappings of peers
     nb::CommDevice view{};
+    nb::CommDevice view_on_device{};  // what d_view holds (upload_view skips identical writes)
+    bool view_uploaded = false;
     nb::CommDevice* d_view = nullptr;
     uint64_t* d_win_table = nullptr;
     uint64_t* d_epoch = nullptr;
@@ -396,7 +398,14 @@ void upload_view(nimbleComm* c) {
     c->view.epoch = c->d_epoch;
     const char* t = std::getenv("NIMBLE_TIMEOUT_MS");
     c->view.timeout_ms = t && *t ? static_cast<uint32_t>(std::atoi(t)) : 60000u;
+    // Only when it changed: a config change that is host-side only (pull
+    // mode, chunk sizes of direct items, LL limit) then touches no device
+    // memory -- no stream operation that could queue behind a co-resident
+    // peer's running engine (see internal_stream).
+    if (c->view_uploaded && std::memcmp(&c->view_on_device, &c->view, sizeof c->view) == 0) return;
     h2d(c, c->d_view, &c->view, sizeof c->view);
+    c->view_on_device = c->view;
+    c->view_uploaded = true;
 }
 
 constexpr uint32_t kMaxWindows = 256;
