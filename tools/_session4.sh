@@ -1,13 +1,15 @@
-# round-2 4-GPU session: relay ring geometry (development aid)
+# final 4-GPU evidence with the final binary (development aid)
 mkdir -p gpurun_out
-O=gpurun_out/s4l
+O=gpurun_out/s4z
 TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
-for g in "0 0" "131072 33554432" "262144 67108864"; do
-  set -- $g
-  if [ "$1" = "0" ]; then E=""; else E="SWEEP_PIPE_CHUNK=$1 SWEEP_P2P_BUFFER=$2"; fi
-  env $E SWEEP_NCCL=0 SWEEP_CASES=c1 timeout 400 $TR --nproc-per-node 3 --master-port 29740 tools/sweeps.py > ${O}_c1_$1.jsonl 2> ${O}_c1_$1.err
-  env $E SWEEP_NCCL=0 SWEEP_CASES=c2,cal timeout 600 $TR --nproc-per-node 4 --master-port 29741 tools/sweeps.py > ${O}_c2_$1.jsonl 2> ${O}_c2_$1.err
-  echo "geometry $1 $2: $(grep -c '^{' ${O}_c1_$1.jsonl) + $(grep -c '^{' ${O}_c2_$1.jsonl) rows"
+for n in 2 4; do
+  timeout 400 $TR --nproc-per-node $n --master-port 2975$n bench.py --gpus $n --steps 20 --warmup 5 > ${O}_bench_n$n.json 2> ${O}_bench_n$n.err
+  echo "bench n$n: $(cut -c1-160 ${O}_bench_n$n.json)"
 done
-TRACE_CASE=relay TRACE_PULL=0 TRACE_KIB=65536 timeout 300 $TR --nproc-per-node 3 --master-port 29742 tools/trace_probe.py > ${O}_trace_relay.txt 2>&1
+timeout 400 $TR --nproc-per-node 4 --master-port 29760 bench.py --gpus 4 --steps 20 --warmup 5 --fresh-matrix --no-e2e --no-baselines > ${O}_bench_fresh_n4.json 2> ${O}_bench_fresh_n4.err
+M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,nvltx__bytes.sum,nvlrx__bytes.sum,nvltx__bytes_data_user.sum,nvlrx__bytes_data_user.sum,nvltx__bytes_data_protocol.sum,nvlrx__bytes_data_protocol.sum"
+for mib in 256 64; do
+  NIMBLE_TIMEOUT_MS=180000 NIMBLE_PDL=0 timeout 400 ncu --metrics $M -k regex:exchange_kernel --launch-skip 7 --launch-count 1 --csv python tools/ncu_clique.py --gpus 4 --groups 2 --hot 3 --per-rank-mib $mib > ${O}_ncu_hot_$mib.csv 2> ${O}_ncu_hot_$mib.err
+  echo "ncu hot $mib rc=$?"
+done
 echo done
