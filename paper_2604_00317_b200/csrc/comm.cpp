@@ -577,6 +577,13 @@ void setup_common(nimbleComm* c) {
         CUDA_TRY(cudaMemPoolCreate(&c->pool, &props));
         uint64_t keep = ~0ull;
         CUDA_TRY(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        // No allocation may wait on another stream's pending free (the
+        // allocator's "internal dependencies"): on a device hosting several
+        // ranks, the stream holding that free can share a hardware queue with
+        // a peer's spinning engine (see internal_stream).  Freed blocks are
+        // reused once their frees have completed.
+        int no = 0;
+        CUDA_TRY(cudaMemPoolSetAttribute(c->pool, cudaMemPoolReuseAllowInternalDependencies, &no));
         void* warm = nullptr;
         CUDA_TRY(cudaMallocFromPoolAsync(&warm, 16ull << 20, c->pool, c->aux));
         CUDA_TRY(cudaFreeAsync(warm, c->aux));
