@@ -770,6 +770,17 @@ int window_of(const nimbleComm* c, uint64_t ptr, uint64_t n) {
     return -1;
 }
 
+// NIMBLE_PUSH_DISTANCES=mask (experiment, 0 = off): receivers do not ask
+// senders at ring distance d (me - s mod R) with bit d set to be pulled from,
+// so those pairs are pushed -- a per-pair push / pull split of balanced ports.
+uint64_t push_distances() {
+    static const uint64_t m = [] {
+        const char* e = std::getenv("NIMBLE_PUSH_DISTANCES");
+        return static_cast<uint64_t>(e && *e ? std::strtoull(e, nullptr, 0) : 0);
+    }();
+    return m;
+}
+
 // Where each incoming segment lands: a registered window (zero copy) or the
 // self ring (staged); where each outgoing segment lives (registered windows
 // can be pulled by their receiver); whether this rank asks to pull.
@@ -848,7 +859,8 @@ void fill_posts(nimbleComm* c, RankBuffers& rb, const PlanResult& plan) {
             p.win = static_cast<uint32_t>(w);
             p.off = rb.recv_ptr[s] - c->windows[static_cast<size_t>(w)].base;
         }
-        if (rb.pull && !relayed[static_cast<size_t>(s)]) p.mode |= kPostPullRequest;
+        const int dist = (rb.me - s + rb.R) % rb.R;  // NIMBLE_PUSH_DISTANCES: experiment, see push_distances()
+        if (rb.pull && !relayed[static_cast<size_t>(s)] && !((push_distances() >> dist) & 1)) p.mode |= kPostPullRequest;
         rb.recv_post[static_cast<size_t>(s)] = p;
     }
 }
