@@ -195,6 +195,8 @@ def main():
         comm.set_config(ll_max=int(os.environ["SWEEP_LL_MAX"]))
     if os.environ.get("SWEEP_PUSH_CHUNK"):
         comm.set_config(push_chunk=int(os.environ["SWEEP_PUSH_CHUNK"]))
+    if os.environ.get("SWEEP_CTAS"):
+        comm.set_config(ctas=int(os.environ["SWEEP_CTAS"]))
     if os.environ.get("SWEEP_PIPE_CHUNK"):  # relay staging geometry (pipe_chunk, p2p_buffer)
         comm.set_config(pipe_chunk=int(os.environ["SWEEP_PIPE_CHUNK"]),
                         p2p_buffer=int(os.environ.get("SWEEP_P2P_BUFFER", str(10 << 20))))
