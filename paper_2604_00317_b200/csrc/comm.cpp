@@ -1683,7 +1683,9 @@ nimbleResult_t nimbleCommGetAsyncError(nimbleComm_t c, nimbleResult_t* err) {
                                      "relay routes need a registered receive buffer",
                                      "timeout waiting for a relay to drain",
                                      "a post was overwritten before it was read (protocol violation)",
-                                     "timeout on a low-latency (LL) slot"};
+                                     "timeout on a low-latency (LL) slot",
+                                     "a work item fell outside its segment or staging slot (scheduler bug; nothing "
+                                     "was written)"};
         nb::g_last_error = code < sizeof what / sizeof what[0] ? what[code] : "unknown device error";
         // where: peer (0xff = unknown; bit 7 = the other direction: a pull, or
         // an LL receive) and the epoch's low 16 bits

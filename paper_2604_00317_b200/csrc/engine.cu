@@ -144,6 +144,7 @@ enum AsyncCode : uint32_t {
     kErrFinalTimeout = 7,
     kErrPostLost = 8,  // a post was overwritten in a way the protocol does not allow
     kErrLLTimeout = 9,   // an LL slot never filled (or its receiver never drained the previous one)
+    kErrBounds = 10,     // a work item's byte range falls outside its segment or staging slot (scheduler bug)
 };
 
 // Latch the first async error of the comm: status[0] = code, status[1] =
@@ -226,6 +227,7 @@ struct SharedState {
     uint64_t sig_empty[kSig];  // signal warp -> producer
     SigDesc sig[kSig];
     uint64_t seg_base[kMaxRanks * kMaxRanks];  // (receiver, sender) -> resolved segment base
+    uint64_t seg_bytes[kMaxRanks * kMaxRanks]; // (receiver, sender) -> the segment's byte count (bounds checks)
     uint32_t seg_mode[kMaxRanks * kMaxRanks];  // 0 = unresolved
     uint64_t send_base[kMaxRanks];             // sender -> its registered send segment (pull)
     uint32_t send_mode[kMaxRanks];             // 0 = unresolved
@@ -312,6 +314,7 @@ __device__ bool resolve(SharedState& sh, const LaunchArgs& a, int d, int s) {
             return false;
         }
         sh.seg_base[key] = 0;
+        sh.seg_bytes[key] = a.send_bytes[d];
         sh.seg_mode[key] = kPostZeroCopy | kPostPullRequest;
         c->scratch[2 + d] = kDecidePull;
         return true;
@@ -326,6 +329,7 @@ __device__ bool resolve(SharedState& sh, const LaunchArgs& a, int d, int s) {
         }
     }
     sh.seg_base[key] = (mode & 0xf) == kPostZeroCopy ? c->win_table[win * kMaxRanks + d] + off : 0;
+    sh.seg_bytes[key] = v.bytes;
     sh.seg_mode[key] = mode;
     if (direct)  // record, for the epilogue, whether d pulls my segment or takes pushes
         c->scratch[2 + d] = ((mode & kPostPullRequest) && a.send_posts[d].mode == kSendRegistered) ? kDecidePull
@@ -394,6 +398,16 @@ __device__ __forceinline__ void count_item(const CommDevice* c, int kind, int pe
 
 enum Prep { kGo, kSkip };
 
+// Every item's byte range must lie inside the segment (or staging slot) it
+// addresses -- true by construction of the schedule; checked anyway, on
+// every item, because a violation would write another rank's memory.  A few
+// integer compares per item (items are 8-64 KiB).
+__device__ __forceinline__ bool in_bounds(const CommDevice* c, uint64_t off, uint32_t bytes, uint64_t limit) {
+    if (off + bytes <= limit) return true;
+    atomicCAS(c->status, 0u, static_cast<uint32_t>(kErrBounds));
+    return false;
+}
+
 // Producer: the item's source, destination and end-of-item actions.  kSkip
 // when the item has nothing to do (pull granted / declined) or a wait failed
 // (the error is latched in the status word).
@@ -410,6 +424,7 @@ __device__ Prep prepare(SharedState& sh, const LaunchArgs& a, const Item& it, ui
         const int s = it.peer;
         if (!resolve_send(sh, a, s)) return kSkip;
         if (sh.send_mode[s] != kSendRegistered) return kSkip;  // declined: s pushes instead
+        if (!in_bounds(c, it.src, it.bytes, a.posts[s].bytes)) return kSkip;  // inside s's segment for me
         src = sh.send_base[s] + it.src;  // pulled[] is counted once per CTA (epilogue)
         return kGo;
     }
@@ -419,11 +434,13 @@ __device__ Prep prepare(SharedState& sh, const LaunchArgs& a, const Item& it, ui
         if (it.kind == kPush) {
             if (!resolve(sh, a, d, me)) return kSkip;
             if (pull_granted_to(sh, a, d)) return kSkip;  // d pulls this range itself
+            if (!in_bounds(c, it.dst, it.bytes, a.send_bytes[d])) return kSkip;  // inside my segment for d
             if ((sh.seg_mode[d * kMaxRanks + me] & 0xf) == kPostZeroCopy) {
                 dst = sh.seg_base[d * kMaxRanks + me] + it.dst;  // done[] is counted once per CTA (epilogue)
                 return kGo;
             }
         }
+        if (!in_bounds(c, 0, it.bytes, a.pipe_chunk)) return kSkip;  // one staging slot
         const uint32_t slot = it.seq % a.slots;
         if (it.seq >= a.slots &&
             !wait_ge(ctrl_flag(a, me, FlagLayout::consumed_off(R, d, host, slot)), tag_of(a.epoch, it.seq - a.slots), c,
@@ -462,6 +479,7 @@ __device__ Prep prepare(SharedState& sh, const LaunchArgs& a, const Item& it, ui
         atomicCAS(c->status, 0u, static_cast<uint32_t>(kErrRelayToStaged));
         return kSkip;
     }
+    if (!in_bounds(c, it.dst, it.bytes, sh.seg_bytes[d * kMaxRanks + s])) return kSkip;  // inside d's segment for s
     dst = sh.seg_base[d * kMaxRanks + s] + it.dst;
     return kGo;
 }
